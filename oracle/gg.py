@@ -1,0 +1,163 @@
+"""Group Generator with Group Buffer, Global Division and the slowdown filter.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__).
+
+PAPER.md passages followed, in the paper's order of operations:
+  * request: "When a worker needs to perform a synchronization, it just needs to
+    contact GG"; the GG "generates groups in a serial manner"
+  * request counter c_w: "records how many times the worker requires a group"
+    (P:1184-1185); incremented at request time (reading R10)
+  * Group Buffer: "the ordered list of groups that include the corresponding
+    worker"; a non-empty GB serves its first group
+  * Global Division: "divides all current workers with empty GBs into several
+    non-conflicting groups", called "only when the initiator's GB is empty"
+    
+  * slowdown filter: a GD admits w only if c_i - c_w < C_thres
+  * lock vector: "a bit vector indicating whether each worker is currently
+    performing a P-Reduce"; set on grant, released by the ack after P-Reduce
+    
+
+Readings (= SURVEY §8(c) c.2): candidates are workers with empty GB,
+passing the filter, not retired (R7, R19); the random partition is splitmix64
++ Fisher-Yates, the initiator's group first, chunks of k, the last one possibly
+shorter, no candidates -> singleton (R8); C_thres <= 0 disables the filter (R9).
+"""
+from dataclasses import dataclass, field
+
+_MASK = (1 << 64) - 1
+
+
+def _mix(z):
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & _MASK
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & _MASK
+    z ^= z >> 31
+    return z
+
+
+class ProtocolError(Exception):
+    pass
+
+
+class ConflictError(Exception):
+    pass
+
+
+@dataclass
+class GGState:
+    n: int
+    k: int
+    c_thres: int
+    rng: int                       # splitmix64 state (seed_gd)
+    seq: int = 0                   # next group sequence number
+    gb: list = field(default_factory=list)        # per worker: list of seq (FIFO)
+    counters: list = field(default_factory=list)  # c_w
+    lock: int = 0                  # bit w set while w holds a granted, unfinished group
+    retired: int = 0               # bit w set once w finished its final step
+    retiring: int = 0              # bit w set: retire w when its held group completes
+    handed: list = field(default_factory=list)    # per worker: seq handed out by req, or -1
+    groups: dict = field(default_factory=dict)    # seq -> tuple(members)
+
+    def key(self):
+        return (self.rng, self.seq, tuple(tuple(b) for b in self.gb), tuple(self.counters),
+                self.lock, self.retired, self.retiring, tuple(self.handed),
+                tuple(sorted((s, m) for s, m in self.groups.items())))
+
+
+class GroupGenerator:
+    """The GG of §5 with GB + GD + filter; one instance = one serial decision loop."""
+
+    def __init__(self, n, k, c_thres=4, seed_gd=3):
+        if not (1 <= k <= n):
+            raise ValueError("need 1 <= k <= n")
+        self.s = GGState(n=n, k=k, c_thres=c_thres, rng=seed_gd & _MASK,
+                         gb=[[] for _ in range(n)], counters=[0] * n, handed=[-1] * n)
+        self.trace = []
+        self.gd_calls = 0
+
+    # -- RNG: splitmix64 (next = MIX(state += golden)) -------------------------
+    def _next(self):
+        self.s.rng = (self.s.rng + 0x9E3779B97F4A7C15) & _MASK
+        return _mix(self.s.rng)
+
+    def _global_division(self, i):
+        """partition the idle workers (empty GB), initiator's group first."""
+        s = self.s
+        self.gd_calls += 1
+        cand = []
+        for v in range(s.n):
+            if v == i or s.gb[v] or (s.retired >> v) & 1:
+                continue
+            if s.c_thres > 0 and not (s.counters[i] - s.counters[v] < s.c_thres):
+                continue  # slowdown filter
+            cand.append(v)
+        for q in range(len(cand) - 1, 0, -1):  # Fisher-Yates
+            j = self._next() % (q + 1)
+            cand[q], cand[j] = cand[j], cand[q]
+        chunks = [[i] + cand[:s.k - 1]]
+        rest = cand[s.k - 1:]
+        chunks += [rest[p:p + s.k] for p in range(0, len(rest), s.k)]
+        for ch in chunks:
+            members = tuple(sorted(ch))
+            bits = 0
+            for m in members:
+                bits |= 1 << m
+            if s.lock & bits:  # overlapping groups must be serialized
+                raise ConflictError(f"GD produced a group overlapping a held lock: {members}")
+            s.lock |= bits
+            s.groups[s.seq] = members
+            for m in members:
+                s.gb[m].append(s.seq)
+            s.seq += 1
+
+    def req(self, i):
+        """Synchronization request of worker i. Returns (seq, members)."""
+        s = self.s
+        if not (0 <= i < s.n) or (s.retired >> i) & 1:
+            raise ProtocolError(f"request from invalid or retired worker {i}")
+        if s.handed[i] != -1:
+            raise ProtocolError(f"worker {i} requested again before its group {s.handed[i]} completed")
+        s.counters[i] += 1
+        if not s.gb[i]:
+            self._global_division(i)
+        seq = s.gb[i][0]
+        s.handed[i] = seq
+        self.trace.append(("req", i, seq, s.groups[seq]))
+        return seq, s.groups[seq]
+
+    def done(self, seq):
+        """Completion (ack) of group seq: pop GBs, release lock bits."""
+        s = self.s
+        members = s.groups.pop(seq)
+        for m in members:
+            if not s.gb[m] or s.gb[m][0] != seq:
+                raise ProtocolError(f"group {seq} is not at the head of worker {m}'s GB")
+            if s.handed[m] != seq:
+                raise ProtocolError(f"group {seq} completed before member {m} requested it")
+            s.gb[m].pop(0)
+            s.handed[m] = -1
+            s.lock &= ~(1 << m)
+        self.trace.append(("done", seq))
+        for m in members:  # retire atomically with the completion (reading R19)
+            if (s.retiring >> m) & 1:
+                s.retiring &= ~(1 << m)
+                s.retired |= 1 << m
+                self.trace.append(("retire", m))
+        return members
+
+    def retire(self, w):
+        """Worker w will not request again; GD must never assign it again (reading R19).
+
+        If w holds a group, it retires when that group completes (same decision
+        step), so no GD can pick it between its last completion and retirement.
+        """
+        s = self.s
+        if s.handed[w] != -1:
+            s.retiring |= 1 << w
+        else:
+            s.retired |= 1 << w
+            self.trace.append(("retire", w))
+
+    def gb_depth(self):
+        return max(len(b) for b in self.s.gb)

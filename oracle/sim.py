@@ -1,0 +1,105 @@
+"""Sequential simulator of n workers running alg1 (TEST INFRASTRUCTURE ONLY).
+
+alg1, per worker i and iteration t:
+  Step 1-2  y_i = x_i - eta * grad_i^t
+  Step 3    a group G containing i
+  Step 4    x_g <- (1/|G|) sum_{g in G} y_g for g in G
+Disjoint groups commute exactly (F^G's of non-overlapping G), so a
+step's groups can be applied in any order; the simulator applies them in a
+fixed order. Workers that skip synchronization apply Step 2 only.
+
+Two drivers:
+  * run_lockstep: every worker does step t before any does t+1 (cfg 1-4).
+    Groups come from a static rule or the GG with requests in
+    ascending worker order and every group completed at the end of the step.
+  * replay_trace: an asynchronous run (cfg 5) is replayed from the engine's
+    JSONL decision trace (req / done / retire in GG order): the oracle GG must
+    reproduce every grant, then parameters are updated per completed group in
+    trace order, each member using its own step count t (reading R18).
+Gradients are xi(SEED_G, w, t, j) from rp_inputs (x-independent, reading R14).
+"""
+import numpy as np
+
+from rp_inputs import gen as xi_mod
+from . import schedule as sched_mod
+from .gg import GroupGenerator, ProtocolError
+from .update import fused_group_update
+
+F32 = np.float32
+
+
+def init_replicas(n, n_params, lo=0, hi=None):
+    return {w: xi_mod.x0(w, n_params, lo, hi) for w in range(n)}
+
+
+def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
+                 rule=None, k=None, nodes=None, m=None, c_thres=4, seed_gd=3,
+                 lo=0, hi=None, X=None, first_step=1, gg=None, log=None):
+    """Simulate `steps` lockstep steps; returns (X, log).
+
+    mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter).
+    [lo, hi) restricts the simulated element range (elementwise method, so a
+    slice is computed exactly as in the full run).
+    log: list receiving (t, [groups]) per step, groups as sorted tuples.
+    """
+    hi = n_params if hi is None else hi
+    X = init_replicas(n, n_params, lo, hi) if X is None else X
+    wpg = workers_per_gpu or n
+    log = [] if log is None else log
+    if mode == "gd" and gg is None:
+        gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd)
+    for t in range(first_step, first_step + steps):
+        if mode == "static":
+            groups = [tuple(g) for g in sched_mod.groups_for(rule, t, n=n, k=k, nodes=nodes, m=m)]
+        elif mode == "gd":
+            seen = {}
+            for w in range(n):              # requests in ascending worker order
+                seq, members = gg.req(w)
+                seen[seq] = members
+            groups = [seen[s] for s in sorted(seen)]
+            for s in sorted(seen):          # all groups complete at the end of the step
+                gg.done(s)
+        else:
+            raise ValueError(mode)
+        in_group = set(w for g in groups for w in g)
+        for g in groups:
+            G = {w: xi_mod.grad(w, t, n_params, lo, hi) for w in g}
+            fused_group_update(X, G, g, lr, wpg)
+        for w in range(n):
+            if w not in in_group:           # skip: SGD only (singleton)
+                fused_group_update(X, {w: xi_mod.grad(w, t, n_params, lo, hi)}, (w,), lr, wpg)
+        log.append((t, [tuple(g) for g in groups] + [(w,) for w in range(n) if w not in in_group]))
+    return X, log
+
+
+def replay_trace(events, n, n_params, *, k, c_thres, seed_gd, lr=0.1,
+                 workers_per_gpu=None, lo=0, hi=None):
+    """Replay an async decision trace; returns (X, steps_per_worker).
+
+    events: iterable of dicts {"ev": "req", "w", "seq", "members"} |
+            {"ev": "done", "seq"} | {"ev": "retire", "w"} in GG order.
+    Raises ProtocolError if a recorded grant differs from the oracle GG's.
+    """
+    hi = n_params if hi is None else hi
+    X = init_replicas(n, n_params, lo, hi)
+    wpg = workers_per_gpu or n
+    gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd)
+    t_of = [0] * n
+    for e in events:
+        if e["ev"] == "req":
+            seq, members = gg.req(e["w"])
+            if seq != e["seq"] or tuple(members) != tuple(e["members"]):
+                raise ProtocolError(f"grant mismatch at req w={e['w']}: oracle {seq}:{members} "
+                                    f"vs trace {e['seq']}:{e['members']}")
+        elif e["ev"] == "done":
+            members = gg.done(e["seq"])
+            G = {}
+            for w in members:
+                t_of[w] += 1
+                G[w] = xi_mod.grad(w, t_of[w], n_params, lo, hi)
+            fused_group_update(X, G, members, lr, wpg)
+        elif e["ev"] == "retire":
+            gg.retire(e["w"])
+        else:
+            raise ValueError(e)
+    return X, t_of
