@@ -1,0 +1,248 @@
+/*
+ * rp.h — C ABI of librp, a B200-native Partial All-Reduce (P-Reduce) library.
+ *
+ * Method: Ripples, "Heterogeneity-Aware Asynchronous Decentralized Training"
+ * (arXiv 1909.08029). Citations "P:<line>" are lines of its LaTeX source
+ * (PAPER.md); sections: §3 P-Reduce, §4 Group Generation,
+ * §5 Smart GG, §6 Implementation.
+ *
+ * What one training iteration of worker i does (alg1):
+ *   Step 2  x_i <- x_i - eta * grad_i                       -> rp_step
+ *   Step 3  get a group G containing i                        -> rp_schedule_static[_worker]
+ *                                                                or rp_group_generate
+ *   Step 4  atomically x_g <- (1/|G|) sum_{g in G} x_g         -> rp_preduce (collective)
+ *           and continue once *its own* group is done          -> rp_barrier_free_wait
+ * Steps 2 and 4 run fused in one pass of a CUDA kernel: y_m = x_m - eta*g_m is
+ * never written to memory; the mean of the members' y is written to every
+ * member replica in place.
+ *
+ * Conventions
+ *   - Every function returns int status: RP_OK (0) or a negative RP_E* code.
+ *     No C++ exception or abort crosses this boundary. rp_last_error() gives
+ *     a thread-local message for the last failing call on the calling thread.
+ *   - Device pointers (x, g, grad) are BORROWED: the caller (e.g. a torch
+ *     tensor) owns them and keeps them alive until rp_finalize. They must be
+ *     16-byte aligned fp32 arrays of n_params elements on the worker's GPU.
+ *   - The context, its CUDA streams, events and peer mappings are owned by the
+ *     library and released by rp_finalize.
+ *   - Calls for distinct workers may come from different host threads; the
+ *     Group Generator is serialized internally ("generates groups in a serial
+ *     manner").
+ *   - Worker placement (reading R6): worker w lives on GPU w / workers_per_gpu.
+ *     One process drives one GPU (rank = GPU index); that process binds and
+ *     drives exactly the workers of its GPU.
+ */
+#ifndef RP_H
+#define RP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RP_ABI_VERSION 1
+#define RP_MAX_WORLD 64 /* lock vector is one uint64_t, one bit per worker */
+#define RP_MAX_GROUP 16 /* largest group a P-Reduce accepts */
+#define RP_MAX_GPUS 8   /* GPUs of one NVSwitch node */
+
+/* ---- status codes ---------------------------------------------------------- */
+#define RP_OK 0
+#define RP_EINVAL (-1)    /* bad argument (range, alignment, device)                    */
+#define RP_ESTATE (-2)    /* call not valid in the worker's current state               */
+#define RP_EPROTO (-3)    /* collective contract broken: members disagree on the group,
+                             or the group is not the one the GG handed out      */
+#define RP_ECONFLICT (-4) /* a member already holds an unfinished group: atomicity
+                             violation. Never happens under GD / static.    */
+#define RP_ETIMEOUT (-5)  /* wait timed out; rp_last_error() names missing members      */
+#define RP_ECUDA (-6)     /* CUDA runtime error (message in rp_last_error)              */
+#define RP_ENOMEM (-7)
+#define RP_ENODEV (-8)    /* operation needs a GPU but the context is host-only         */
+
+/* ---- configuration ----------------------------------------------------------- */
+#define RP_FLAG_TRACE 0x1       /* keep the JSONL decision trace (rp_trace_open)       */
+#define RP_FLAG_TIMING 0x2      /* bracket every kernel launch with CUDA timing events
+                                   on its own stream (rp_timing_read)                   */
+
+#define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
+#define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */
+
+typedef struct rp_config {
+  int32_t world;           /* n workers, 1..RP_MAX_WORLD                                 */
+  int32_t n_gpus;          /* GPUs in the job; 0 = host-only context (schedules + GG)    */
+  int64_t n_params;        /* N, fp32 elements per replica (flat), > 0      */
+  int32_t workers_per_gpu; /* wpg; world == n_gpus * wpg when n_gpus > 0                 */
+  int32_t rank;            /* this process's GPU index in [0, n_gpus)                    */
+  int32_t device;          /* CUDA device ordinal this process drives                    */
+  int32_t group_size;      /* k for Global Division and SHIFT_K, 1..RP_MAX_GROUP         */
+  int32_t c_thres;         /* slowdown filter c_i - c_w < C_thres; <= 0 = off   */
+  int32_t nodes;           /* PAPER4 node count (world = nodes * m); 0 = n_gpus          */
+  uint64_t seed_gd;        /* splitmix64 seed of the GD random partition (reading R8)    */
+  int32_t flags;           /* RP_FLAG_*                                                  */
+  int32_t reserved[7];
+} rp_config;
+
+/* One group: members ascending. seq >= 0: granted by the GG (creation order);
+ * seq < 0: a static-schedule group (pure function of rule, step, members). */
+typedef struct rp_group {
+  int64_t seq;
+  int32_t size;
+  int32_t members[RP_MAX_GROUP];
+} rp_group;
+
+typedef struct rp_stats {
+  int64_t groups_launched;    /* P-Reduce groups executed (including singletons)       */
+  int64_t singleton_groups;   /* |G| = 1: SGD only                                      */
+  int64_t cross_gpu_groups;   /* groups whose members span more than one GPU           */
+  int64_t kernel_launches;    /* CUDA kernels this context launched                    */
+  int64_t gd_calls;           /* Global Divisions run by the GG                         */
+  int64_t gg_requests;        /* rp_group_generate calls                                */
+  int64_t max_gb_depth;       /* deepest Group Buffer seen                              */
+  int64_t lock_assertions;    /* conflict checks performed                              */
+  int64_t bytes_hbm;          /* algorithmic HBM bytes moved by launched parts          */
+  int64_t bytes_nvlink;       /* algorithmic NVLink bytes read by this GPU              */
+} rp_stats;
+
+/* Device time of this context's P-Reduce kernel launches (RP_FLAG_TIMING),
+ * from CUDA events recorded on the launching stream around each launch. */
+typedef struct rp_timing {
+  int64_t launches;           /* completed launches accumulated                        */
+  double total_ms;            /* sum of per-launch durations                           */
+  double min_ms, max_ms;
+  int64_t bytes_hbm;          /* algorithmic HBM bytes of those launches               */
+  int64_t bytes_nvlink;       /* algorithmic NVLink bytes of those launches            */
+} rp_timing;
+
+typedef struct rp_ctx rp_ctx;
+
+/* ---- lifecycle ----------------------------------------------------------------- */
+
+/* Create a context (north star rp_init(world, n_params)). With n_gpus > 0 it
+ * selects cfg->device, creates one stream per local worker and the events,
+ * and zeroes the Group Generator state (Group Buffers, counters c_w, lock
+ * vector, RNG = seed_gd). Errors: RP_EINVAL (world not in [1,64],
+ * n_params <= 0, group_size not in [1,16], world != n_gpus*wpg, rank/device
+ * out of range), RP_ECUDA, RP_ENOMEM. */
+int rp_init(const rp_config* cfg, rp_ctx** out);
+
+/* Release streams, events, peer mappings and the context. Does not free the
+ * borrowed replica / gradient buffers. Waits for this context's GPU work. */
+int rp_finalize(rp_ctx* ctx);
+
+/* Register worker w's flat replica x (read-write) and default gradient
+ * buffer g (read-only, may be NULL). Both are device pointers on this
+ * process's GPU, 16-byte aligned, n_params fp32 each; w must belong to this
+ * rank (w / wpg == rank). Errors: RP_EINVAL, RP_ENODEV. */
+int rp_bind_worker(rp_ctx* ctx, int32_t w, float* x_dev, const float* g_dev);
+
+/* The CUDA stream (cudaStream_t as void*) on which worker w's work is
+ * ordered. Producing w's gradient on this stream makes rp_preduce wait for
+ * it; after rp_barrier_free_wait(w, RP_WAIT_DEVICE), work on this stream sees
+ * the averaged replica. Library-owned unless replaced by rp_set_worker_stream. */
+int rp_worker_stream(rp_ctx* ctx, int32_t w, void** stream_out);
+int rp_set_worker_stream(rp_ctx* ctx, int32_t w, void* stream);
+
+/* ---- Step 3: group determination -------------------------------------------------- */
+
+/* Static schedule: a pure function of (rule, config, step), the
+ * same on every caller. Fills group_of[w] = index of w's group in
+ * this step or -1 if w skips synchronization ("-" cells), and
+ * *n_groups. group_of must hold `world` entries (caller-owned).
+ * RP_SCHED_PAPER4 needs world = nodes * m with m = world / nodes.
+ * Errors: RP_EINVAL (unknown rule, rule incompatible with the config). */
+int rp_schedule_static(rp_ctx* ctx, int32_t rule, int64_t step, int32_t* group_of,
+                       int32_t* n_groups);
+
+/* Worker w's group in this step as an rp_group (size 1 when w skips: an
+ * SGD-only "singleton" P-Reduce). seq = -(1 + step*world + members[0]). */
+int rp_schedule_static_worker(rp_ctx* ctx, int32_t rule, int64_t step, int32_t w,
+                              rp_group* out);
+
+/* Dynamic group generation (GG request, §5.1-§5.3): c_w += 1; if
+ * w's Group Buffer is non-empty return its head, else run a Global Division
+ * over workers with empty GB, passing the slowdown filter and not retired,
+ * push the groups to their members' GBs (lock bits set) and return w's.
+ * Serialized by an internal mutex; appends {"ev":"req"} to the trace.
+ * Errors: RP_ESTATE (w still holds an unfinished group, or w retired), RP_EINVAL.
+ * Multi-process jobs: every rank runs the same deterministic GG; lockstep
+ * callers must issue requests in the same order on every rank. */
+int rp_group_generate(rp_ctx* ctx, int32_t w, rp_group* out);
+
+/* Acknowledge completion of GG group `seq` that this process does not
+ * execute: pops it from its members' Group Buffers and clears
+ * their lock bits, exactly as rp_barrier_free_wait does for local groups.
+ * Used by ranks that replicate the deterministic GG in lockstep runs and by
+ * host-only contexts. Errors: RP_EPROTO (unknown group, not at the head of a
+ * member's GB, or a member that never requested it). */
+int rp_gg_release(rp_ctx* ctx, int64_t seq);
+
+/* Worker w will not request again after its current group (reading R19: a
+ * finished worker must never be put into a Global Division). */
+int rp_retire(rp_ctx* ctx, int32_t w);
+
+/* ---- Step 2 + 4: fused SGD + P-Reduce ---------------------------------------------- */
+
+/* Stage worker w's SGD update x_w <- x_w - lr * grad for its next
+ * rp_preduce (alg1 step 2). grad = NULL uses the bound g buffer.
+ * The pointer is borrowed until w's group completes. A member without a
+ * staged step contributes y = x. Errors: RP_ESTATE (already staged),
+ * RP_EINVAL (misaligned / no buffer). */
+int rp_step(rp_ctx* ctx, int32_t w, const float* grad_dev, float lr);
+
+/* Collective arrival of worker w at group g (alg1 step 4). Every
+ * member must call with an identical group. The last local
+ * arriver enqueues the fused kernel on its worker stream after the other
+ * members' streams (events, no host blocking). The kernel computes, per
+ * element j, y_m = x_m[j] - lr_m*g_m[j] for m in G, the pinned fp32 sum
+ * (reading R1), xbar = sum / |G|, and writes xbar to every member replica;
+ * non-members are untouched (F^G_uu = 1). |G| = 1 is an SGD step.
+ * Errors: RP_EPROTO (w not in g, members disagree, or a GG group other than
+ * the one handed to w), RP_ESTATE (w's previous group not waited),
+ * RP_ECONFLICT, RP_ECUDA. */
+int rp_preduce(rp_ctx* ctx, int32_t w, const rp_group* g);
+
+/* Launch batching (one kernel per lockstep step). Between rp_batch_begin and
+ * rp_batch_end, groups whose local members have all arrived are queued
+ * instead of launched; rp_batch_end launches all queued groups as ONE fused
+ * kernel (disjoint groups run concurrently inside it). Outside a
+ * batch every ready group launches at once. A wait on a queued group before
+ * rp_batch_end returns RP_ESTATE. */
+int rp_batch_begin(rp_ctx* ctx);
+int rp_batch_end(rp_ctx* ctx);
+
+/* Group-local completion: never a world barrier.
+ * timeout_us >= 0: block the calling host thread until w's group is done on
+ *   the device (or RP_ETIMEOUT, naming members that never arrived).
+ * timeout_us == RP_WAIT_DEVICE: do not block the host; w's worker stream is
+ *   already ordered after the group's kernel. Requires the group launched.
+ * Either way, when the last member of a group has waited, the GG releases it
+ * (Group Buffer pop, lock bits clear, {"ev":"done"} in the trace). */
+#define RP_WAIT_DEVICE (-1)
+int rp_barrier_free_wait(rp_ctx* ctx, int32_t w, int64_t timeout_us);
+
+/* ---- observability ------------------------------------------------------------------ */
+int rp_stats_get(rp_ctx* ctx, rp_stats* out);
+/* Block until every timed launch so far has completed, return their sums and
+ * reset the accumulator. Errors: RP_ESTATE (context created without
+ * RP_FLAG_TIMING), RP_ECUDA. */
+int rp_timing_read(rp_ctx* ctx, rp_timing* out);
+/* Start writing the JSONL decision trace (req / done / retire in GG order)
+ * to `path` (truncates). The oracle replays it (tests/). */
+int rp_trace_open(rp_ctx* ctx, const char* path);
+const char* rp_last_error(void);
+const char* rp_strerror(int status);
+int rp_abi_version(void);
+
+/* ---- synthetic inputs (harness kernel, not part of the method) ----------------------- */
+/* dst[i] = xi(seed, w, t, j0 + i) for i < n on `stream` (cudaStream_t as void*),
+ * the counter-based generator of DESIGN.md "Input recipe" (splitmix64
+ * finalizer; bit-identical to rp_inputs/gen.py). dst must be 4-byte aligned
+ * device memory. Errors: RP_EINVAL, RP_ECUDA. */
+int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RP_H */

@@ -1,0 +1,654 @@
+// librp C ABI and the group-execution engine (see include/rp.h for the contract).
+//
+// Engine model (alg1 step 4; concurrency P:639-641; group-local
+// completion P:485-487):
+//  - every local worker owns a CUDA stream; its gradient is produced there;
+//  - rp_preduce records an "arrived" event on the arriving worker's stream;
+//  - the last local arriver makes its own stream wait on the other members'
+//    arrival events and enqueues the fused kernel there, then every other
+//    member's stream waits on the group's completion event. No host blocking,
+//    no global barrier: disjoint groups run concurrently on different streams;
+//  - rp_barrier_free_wait either blocks the host on the member's completion
+//    event or (RP_WAIT_DEVICE) relies on stream order; when the last member
+//    has waited the GG releases the group (Group Buffer pop, lock bits clear,
+//    P:741-742) and the trace logs "done".
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <algorithm>
+#include <new>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "rp_internal.h"
+
+namespace rp {
+namespace {
+thread_local std::string t_last_error;
+}
+
+int fail(int code, const std::string& msg) {
+  t_last_error = msg;
+  return code;
+}
+
+}  // namespace rp
+
+using rp::fail;
+
+namespace {
+
+struct WorkerSlot {
+  bool local = false;
+  bool bound = false;
+  float* x = nullptr;
+  const float* g = nullptr;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_arrive = nullptr;  // worker's inputs are ready (recorded at rp_preduce)
+  cudaEvent_t ev_group = nullptr;   // completion of a group this worker launched
+  cudaEvent_t ev_done = nullptr;    // this worker's group is done, in its stream order
+  bool staged = false;
+  const float* grad = nullptr;
+  float lr = 0.f;
+  bool in_group = false;  // arrived at a group and not yet waited
+  int64_t seq = 0;
+};
+
+struct ActiveGroup {
+  rp_group g{};
+  uint64_t members_mask = 0;
+  uint64_t local_mask = 0;
+  uint64_t arrived = 0;
+  uint64_t waited = 0;
+  bool launched = false;
+  const float* grad[RP_MAX_GROUP] = {};
+  float lr[RP_MAX_GROUP] = {};
+};
+
+std::string members_str(const rp_group& g, uint64_t mask_filter = ~0ull) {
+  std::ostringstream os;
+  os << "[";
+  bool first = true;
+  for (int i = 0; i < g.size; ++i) {
+    if (!((mask_filter >> g.members[i]) & 1)) continue;
+    if (!first) os << ",";
+    os << g.members[i];
+    first = false;
+  }
+  os << "]";
+  return os.str();
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(RP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                 \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+}  // namespace
+
+struct rp_ctx {
+  rp_config cfg{};
+  bool has_gpu = false;
+  std::mutex mu;
+  std::condition_variable cv;
+  WorkerSlot w[RP_MAX_WORLD];
+  std::map<int64_t, ActiveGroup> active;
+  uint64_t inflight = 0;  // engine lock vector: members of launched, un-waited groups
+  rp::GGState gg{};
+  rp_stats stats{};
+  FILE* trace = nullptr;
+  bool batching = false;
+  std::vector<int64_t> ready;  // groups queued inside a batch
+  struct Timed {
+    cudaEvent_t start, stop;
+    int64_t bytes_hbm, bytes_nvlink;
+  };
+  std::vector<Timed> timed;           // recorded, not yet read
+  std::vector<cudaEvent_t> event_pool;  // timing events for reuse
+};
+
+namespace {
+
+void trace_line(rp_ctx* c, const std::string& s) {
+  if (!c->trace) return;
+  std::fputs(s.c_str(), c->trace);
+  std::fputc('\n', c->trace);
+  std::fflush(c->trace);
+}
+
+std::string group_json(const rp_group& g) {
+  std::ostringstream os;
+  os << "\"seq\":" << g.seq << ",\"members\":[";
+  for (int i = 0; i < g.size; ++i) os << (i ? "," : "") << g.members[i];
+  os << "]";
+  return os.str();
+}
+
+bool worker_ok(const rp_ctx* c, int32_t w) { return w >= 0 && w < c->cfg.world; }
+
+int check_group(const rp_ctx* c, const rp_group* g, uint64_t* mask) {
+  if (!g || g->size < 1 || g->size > RP_MAX_GROUP) return fail(RP_EINVAL, "group size out of range");
+  uint64_t m = 0;
+  for (int i = 0; i < g->size; ++i) {
+    const int v = g->members[i];
+    if (v < 0 || v >= c->cfg.world) return fail(RP_EINVAL, "group member out of range");
+    if (i > 0 && v <= g->members[i - 1]) return fail(RP_EINVAL, "group members must be strictly ascending");
+    m |= 1ull << v;
+  }
+  *mask = m;
+  return RP_OK;
+}
+
+bool same_group(const rp_group& a, const rp_group& b) {
+  if (a.seq != b.seq || a.size != b.size) return false;
+  for (int i = 0; i < a.size; ++i)
+    if (a.members[i] != b.members[i]) return false;
+  return true;
+}
+
+// GG release of a completed group + trace (caller holds mu).
+int release_gg_group(rp_ctx* c, int64_t seq) {
+  rp_group rel{};
+  const int rc = rp::gg_done(&c->gg, seq, &rel);
+  if (rc != RP_OK) return rc;
+  trace_line(c, "{\"ev\":\"done\",\"seq\":" + std::to_string(seq) + "}");
+  return RP_OK;
+}
+
+cudaEvent_t timing_event(rp_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// Enqueue ONE fused kernel for a set of ready groups whose members are all
+// local (caller holds mu). The kernel runs on the stream of the lowest local
+// member after every member's arrival event; every member's stream is then
+// ordered after the kernel and records its own completion event.
+int launch_groups(rp_ctx* c, const std::vector<int64_t>& seqs) {
+  if (seqs.empty()) return RP_OK;
+  uint64_t all = 0;
+  for (int64_t q : seqs) {
+    ActiveGroup& a = c->active.at(q);
+    if (a.local_mask != a.members_mask)
+      return fail(RP_EINVAL, "group " + members_str(a.g) + " spans GPUs; cross-GPU groups need the peer engine");
+    c->stats.lock_assertions++;
+    if ((c->inflight | all) & a.members_mask)  // a member is still inside another group
+      return fail(RP_ECONFLICT, "atomicity violation: members " + members_str(a.g, c->inflight | all) +
+                                    " hold an unfinished group");
+    all |= a.members_mask;
+  }
+  int launcher = __builtin_ctzll(all);
+  WorkerSlot& L = c->w[launcher];
+  for (int m = 0; m < RP_MAX_WORLD; ++m)
+    if (((all >> m) & 1) && m != launcher) CUDA_TRY(cudaStreamWaitEvent(L.stream, c->w[m].ev_arrive, 0));
+  // One launch per distinct group size (kernels are specialized on k); each
+  // launch packs up to kMaxTasks groups / kMaxTaskMembers members.
+  std::map<int, std::vector<int64_t>> by_size;
+  for (int64_t q : seqs) by_size[c->active.at(q).g.size].push_back(q);
+  for (auto& kv : by_size) {
+    const std::vector<int64_t>& list = kv.second;
+    size_t gi = 0;
+    while (gi < list.size()) {
+      rp::MultiTask t{};
+      int nm = 0;
+      int64_t bytes = 0;
+      while (gi < list.size() && t.ngroups < rp::kMaxTasks && nm + kv.first <= rp::kMaxTaskMembers) {
+        ActiveGroup& a = c->active.at(list[gi]);
+        t.group_k[t.ngroups] = a.g.size;
+        t.group_first[t.ngroups] = nm;
+        for (int i = 0; i < a.g.size; ++i) {
+          t.x[nm] = c->w[a.g.members[i]].x;
+          t.g[nm] = a.grad[i];
+          t.lr[nm] = a.lr[i];
+          bytes += (a.grad[i] ? 12 : 8) * c->cfg.n_params;
+          ++nm;
+        }
+        t.ngroups++;
+        if (a.g.size == 1) c->stats.singleton_groups++;
+        c->stats.groups_launched++;
+        ++gi;
+      }
+      const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (timing) {
+        e0 = timing_event(c);
+        e1 = timing_event(c);
+        if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
+        CUDA_TRY(cudaEventRecord(e0, L.stream));
+      }
+      std::string err;
+      const int rc = rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
+      if (rc != RP_OK) return fail(rc, err);
+      if (timing) {
+        CUDA_TRY(cudaEventRecord(e1, L.stream));
+        c->timed.push_back({e0, e1, bytes, 0});
+      }
+      c->stats.kernel_launches++;
+      c->stats.bytes_hbm += bytes;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
+  for (int m = 0; m < RP_MAX_WORLD; ++m) {
+    if (!((all >> m) & 1)) continue;
+    WorkerSlot& s = c->w[m];
+    if (m != launcher) CUDA_TRY(cudaStreamWaitEvent(s.stream, L.ev_group, 0));
+    CUDA_TRY(cudaEventRecord(s.ev_done, s.stream));
+  }
+  for (int64_t q : seqs) c->active.at(q).launched = true;
+  c->inflight |= all;
+  c->cv.notify_all();
+  return RP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rp_abi_version(void) { return RP_ABI_VERSION; }
+
+const char* rp_last_error(void) { return rp::t_last_error.c_str(); }
+
+const char* rp_strerror(int status) {
+  switch (status) {
+    case RP_OK: return "ok";
+    case RP_EINVAL: return "invalid argument";
+    case RP_ESTATE: return "invalid state";
+    case RP_EPROTO: return "collective protocol error";
+    case RP_ECONFLICT: return "conflicting groups (atomicity violation)";
+    case RP_ETIMEOUT: return "timeout";
+    case RP_ECUDA: return "CUDA error";
+    case RP_ENOMEM: return "out of memory";
+    case RP_ENODEV: return "no GPU in this context";
+    default: return "unknown status";
+  }
+}
+
+int rp_init(const rp_config* cfg, rp_ctx** out) {
+  if (!cfg || !out) return fail(RP_EINVAL, "rp_init: null argument");
+  *out = nullptr;
+  const rp_config& k = *cfg;
+  if (k.world < 1 || k.world > RP_MAX_WORLD) return fail(RP_EINVAL, "rp_init: world must be in [1, 64]");
+  if (k.n_params <= 0) return fail(RP_EINVAL, "rp_init: n_params must be > 0");
+  if (k.group_size < 1 || k.group_size > RP_MAX_GROUP || k.group_size > k.world)
+    return fail(RP_EINVAL, "rp_init: group_size must be in [1, min(16, world)]");
+  if (k.n_gpus < 0 || k.n_gpus > RP_MAX_GPUS) return fail(RP_EINVAL, "rp_init: n_gpus must be in [0, 8]");
+  if (k.n_gpus > 0) {
+    if (k.workers_per_gpu < 1 || k.n_gpus * k.workers_per_gpu != k.world)
+      return fail(RP_EINVAL, "rp_init: world must equal n_gpus * workers_per_gpu");
+    if (k.rank < 0 || k.rank >= k.n_gpus) return fail(RP_EINVAL, "rp_init: rank out of range");
+  }
+  rp_ctx* c = new (std::nothrow) rp_ctx();
+  if (!c) return fail(RP_ENOMEM, "rp_init: allocation failed");
+  c->cfg = k;
+  if (c->cfg.workers_per_gpu < 1) c->cfg.workers_per_gpu = k.world;
+  rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd);
+  if (k.n_gpus > 0) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      delete c;
+      return fail(RP_ENODEV, std::string("rp_init: no CUDA device: ") + cudaGetErrorString(e));
+    }
+    if (k.device < 0 || k.device >= ndev) {
+      delete c;
+      return fail(RP_EINVAL, "rp_init: device out of range");
+    }
+    e = cudaSetDevice(k.device);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "cudaSetDevice");
+    }
+    c->has_gpu = true;
+    const int wpg = c->cfg.workers_per_gpu;
+    for (int w = k.rank * wpg; w < (k.rank + 1) * wpg; ++w) {
+      WorkerSlot& s = c->w[w];
+      s.local = true;
+      if ((e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s.ev_arrive, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s.ev_group, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming)) != cudaSuccess) {
+        rp_finalize(c);
+        return cuda_fail(e, "rp_init: stream/event creation");
+      }
+      s.own_stream = true;
+    }
+  }
+  *out = c;
+  return RP_OK;
+}
+
+int rp_finalize(rp_ctx* c) {
+  if (!c) return RP_OK;
+  if (c->has_gpu) {
+    cudaSetDevice(c->cfg.device);
+    for (auto& t : c->timed) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.stop);
+    }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    for (auto& s : c->w) {
+      if (s.stream) cudaStreamSynchronize(s.stream);
+      if (s.ev_arrive) cudaEventDestroy(s.ev_arrive);
+      if (s.ev_group) cudaEventDestroy(s.ev_group);
+      if (s.ev_done) cudaEventDestroy(s.ev_done);
+      if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+    }
+  }
+  if (c->trace) std::fclose(c->trace);
+  delete c;
+  return RP_OK;
+}
+
+int rp_bind_worker(rp_ctx* c, int32_t w, float* x, const float* g) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "rp_bind_worker: host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "rp_bind_worker: worker not local to this rank");
+  if (!x || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(g) & 15))
+    return fail(RP_EINVAL, "rp_bind_worker: x (and g) must be non-null 16-byte aligned device pointers");
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, x) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+      pa.device != c->cfg.device) {
+    cudaGetLastError();
+    return fail(RP_EINVAL, "rp_bind_worker: x is not device memory of this rank's GPU");
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->w[w].x = x;
+  c->w[w].g = g;
+  c->w[w].bound = true;
+  return RP_OK;
+}
+
+int rp_worker_stream(rp_ctx* c, int32_t w, void** out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "worker not local");
+  *out = c->w[w].stream;
+  return RP_OK;
+}
+
+int rp_set_worker_stream(rp_ctx* c, int32_t w, void* stream) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "worker not local");
+  std::lock_guard<std::mutex> lk(c->mu);
+  WorkerSlot& s = c->w[w];
+  if (s.in_group) return fail(RP_ESTATE, "worker is inside a group");
+  cudaSetDevice(c->cfg.device);
+  if (s.own_stream) {
+    cudaStreamSynchronize(s.stream);
+    cudaStreamDestroy(s.stream);
+  }
+  s.stream = static_cast<cudaStream_t>(stream);
+  s.own_stream = false;
+  return RP_OK;
+}
+
+int rp_schedule_static(rp_ctx* c, int32_t rule, int64_t step, int32_t* group_of, int32_t* n_groups) {
+  if (!c || !group_of || !n_groups) return fail(RP_EINVAL, "null argument");
+  if (rule == RP_SCHED_PAPER4) {
+    const int nodes = c->cfg.nodes > 0 ? c->cfg.nodes : c->cfg.n_gpus;
+    if (nodes < 1 || c->cfg.world % nodes != 0)
+      return fail(RP_EINVAL, "PAPER4 needs world = nodes * m (set cfg.nodes)");
+    return rp::schedule_paper4(nodes, c->cfg.world / nodes, step, group_of, n_groups);
+  }
+  if (rule == RP_SCHED_SHIFT_K) return rp::schedule_shift_k(c->cfg.world, c->cfg.group_size, step, group_of, n_groups);
+  return fail(RP_EINVAL, "unknown schedule rule");
+}
+
+int rp_schedule_static_worker(rp_ctx* c, int32_t rule, int64_t step, int32_t w, rp_group* out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  if (!worker_ok(c, w)) return fail(RP_EINVAL, "worker out of range");
+  int32_t group_of[RP_MAX_WORLD];
+  int32_t ng = 0;
+  const int rc = rp_schedule_static(c, rule, step, group_of, &ng);
+  if (rc != RP_OK) return rc;
+  std::memset(out, 0xff, sizeof(*out));
+  out->size = 0;
+  if (group_of[w] < 0) {
+    out->members[out->size++] = w;
+  } else {
+    for (int v = 0; v < c->cfg.world; ++v)
+      if (group_of[v] == group_of[w]) {
+        if (out->size >= RP_MAX_GROUP) return fail(RP_EINVAL, "static group larger than RP_MAX_GROUP");
+        out->members[out->size++] = v;
+      }
+  }
+  out->seq = -(1 + step * c->cfg.world + out->members[0]);
+  return RP_OK;
+}
+
+int rp_group_generate(rp_ctx* c, int32_t w, rp_group* out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int rc = rp::gg_request(&c->gg, w, out);
+  if (rc != RP_OK) return rc;
+  c->stats.gg_requests++;
+  trace_line(c, "{\"ev\":\"req\",\"w\":" + std::to_string(w) + "," + group_json(*out) + "}");
+  return RP_OK;
+}
+
+int rp_gg_release(rp_ctx* c, int64_t seq) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->active.count(seq)) return fail(RP_ESTATE, "rp_gg_release: group is executed by this process");
+  return release_gg_group(c, seq);
+}
+
+int rp_retire(rp_ctx* c, int32_t w) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int rc = rp::gg_retire(&c->gg, w);
+  if (rc == RP_OK) trace_line(c, "{\"ev\":\"retire\",\"w\":" + std::to_string(w) + "}");
+  return rc;
+}
+
+int rp_step(rp_ctx* c, int32_t w, const float* grad, float lr) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "rp_step: host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "rp_step: worker not local");
+  std::lock_guard<std::mutex> lk(c->mu);
+  WorkerSlot& s = c->w[w];
+  if (!s.bound) return fail(RP_ESTATE, "rp_step: worker not bound");
+  if (s.staged) return fail(RP_ESTATE, "rp_step: a step is already staged for worker " + std::to_string(w));
+  const float* gp = grad ? grad : s.g;
+  if (!gp) return fail(RP_EINVAL, "rp_step: no gradient buffer");
+  if (reinterpret_cast<uintptr_t>(gp) & 15) return fail(RP_EINVAL, "rp_step: gradient must be 16-byte aligned");
+  s.staged = true;
+  s.grad = gp;
+  s.lr = lr;
+  return RP_OK;
+}
+
+int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "rp_preduce: host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "rp_preduce: worker not local");
+  uint64_t mask = 0;
+  int rc = check_group(c, g, &mask);
+  if (rc != RP_OK) return rc;
+  if (!((mask >> w) & 1)) return fail(RP_EPROTO, "rp_preduce: worker " + std::to_string(w) + " not in group");
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->cfg.device);
+  WorkerSlot& s = c->w[w];
+  if (!s.bound) return fail(RP_ESTATE, "rp_preduce: worker not bound");
+  if (s.in_group)
+    return fail(RP_ESTATE, "rp_preduce: worker " + std::to_string(w) + " has not waited for group " +
+                               std::to_string(s.seq));
+  if (g->seq >= 0) {  // GG group: must be the one handed to w
+    const rp::GGGroup* gg = rp::gg_find(&c->gg, g->seq);
+    bool ok = gg && c->gg.handed[w] == g->seq && gg->size == g->size;
+    for (int i = 0; ok && i < g->size; ++i) ok = gg->members[i] == g->members[i];
+    if (!ok) return fail(RP_EPROTO, "rp_preduce: group " + std::to_string(g->seq) + " was not handed to worker " +
+                                        std::to_string(w) + " by the GG");
+  }
+  auto it = c->active.find(g->seq);
+  if (it == c->active.end()) {
+    ActiveGroup a;
+    a.g = *g;
+    a.members_mask = mask;
+    const int wpg = c->cfg.workers_per_gpu;
+    for (int i = 0; i < g->size; ++i)
+      if (g->members[i] / wpg == c->cfg.rank) a.local_mask |= 1ull << g->members[i];
+    it = c->active.emplace(g->seq, a).first;
+  } else if (!same_group(it->second.g, *g)) {
+    return fail(RP_EPROTO, "rp_preduce: members disagree on group " + std::to_string(g->seq) + ": " +
+                               members_str(it->second.g) + " vs " + members_str(*g));
+  }
+  ActiveGroup& a = it->second;
+  if ((a.arrived >> w) & 1) return fail(RP_EPROTO, "rp_preduce: worker arrived twice");
+  int idx = 0;
+  while (g->members[idx] != w) ++idx;
+  a.grad[idx] = s.staged ? s.grad : nullptr;
+  a.lr[idx] = s.staged ? s.lr : 0.f;
+  CUDA_TRY(cudaEventRecord(s.ev_arrive, s.stream));
+  s.staged = false;
+  s.in_group = true;
+  s.seq = g->seq;
+  a.arrived |= 1ull << w;
+  if ((a.arrived & a.local_mask) == a.local_mask) {
+    if (c->batching) {
+      c->ready.push_back(g->seq);
+      return RP_OK;
+    }
+    return launch_groups(c, {g->seq});
+  }
+  return RP_OK;
+}
+
+int rp_barrier_free_wait(rp_ctx* c, int32_t w, int64_t timeout_us) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "worker not local");
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto deadline = t0 + std::chrono::microseconds(timeout_us < 0 ? 0 : timeout_us);
+  std::unique_lock<std::mutex> lk(c->mu);
+  WorkerSlot& s = c->w[w];
+  if (!s.in_group) return fail(RP_ESTATE, "rp_barrier_free_wait: worker " + std::to_string(w) + " is not in a group");
+  const int64_t seq = s.seq;
+  auto missing = [&](const ActiveGroup& a) { return members_str(a.g, a.members_mask & ~a.arrived); };
+  {
+    ActiveGroup& a = c->active.at(seq);
+    if (!a.launched) {
+      if (timeout_us < 0)
+        return fail(RP_ESTATE, "group " + std::to_string(seq) + " not launched; missing members " + missing(a));
+      if (!c->cv.wait_until(lk, deadline, [&] { return c->active.at(seq).launched; }))
+        return fail(RP_ETIMEOUT, "group " + std::to_string(seq) + " " + members_str(a.g) +
+                                     ": members never arrived: " + missing(c->active.at(seq)));
+    }
+  }
+  if (timeout_us >= 0) {
+    cudaEvent_t ev = s.ev_done;
+    lk.unlock();
+    cudaSetDevice(c->cfg.device);
+    for (;;) {
+      const cudaError_t e = cudaEventQuery(ev);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) return cuda_fail(e, "cudaEventQuery");
+      if (std::chrono::steady_clock::now() >= deadline)
+        return fail(RP_ETIMEOUT, "group " + std::to_string(seq) + " launched but not complete");
+      std::this_thread::yield();
+    }
+    lk.lock();
+  }
+  ActiveGroup& a = c->active.at(seq);
+  s.in_group = false;
+  c->inflight &= ~(1ull << w);
+  a.waited |= 1ull << w;
+  if ((a.waited & a.local_mask) == a.local_mask) {
+    const bool gg_group = seq >= 0;
+    c->active.erase(seq);
+    if (gg_group) return release_gg_group(c, seq);
+  }
+  return RP_OK;
+}
+
+int rp_batch_begin(rp_ctx* c) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->batching) return fail(RP_ESTATE, "rp_batch_begin: already batching");
+  c->batching = true;
+  return RP_OK;
+}
+
+int rp_batch_end(rp_ctx* c) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->batching) return fail(RP_ESTATE, "rp_batch_end: no batch open");
+  c->batching = false;
+  cudaSetDevice(c->cfg.device);
+  std::vector<int64_t> q;
+  q.swap(c->ready);
+  return launch_groups(c, q);
+}
+
+int rp_timing_read(rp_ctx* c, rp_timing* out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  if (!(c->cfg.flags & RP_FLAG_TIMING)) return fail(RP_ESTATE, "context created without RP_FLAG_TIMING");
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->cfg.device);
+  rp_timing r{};
+  r.min_ms = 0;
+  for (auto& t : c->timed) {
+    CUDA_TRY(cudaEventSynchronize(t.stop));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, t.start, t.stop));
+    r.launches++;
+    r.total_ms += ms;
+    r.min_ms = r.launches == 1 ? ms : std::min<double>(r.min_ms, ms);
+    r.max_ms = std::max<double>(r.max_ms, ms);
+    r.bytes_hbm += t.bytes_hbm;
+    r.bytes_nvlink += t.bytes_nvlink;
+    c->event_pool.push_back(t.start);
+    c->event_pool.push_back(t.stop);
+  }
+  c->timed.clear();
+  *out = r;
+  return RP_OK;
+}
+
+int rp_stats_get(rp_ctx* c, rp_stats* out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  *out = c->stats;
+  out->gd_calls = c->gg.gd_calls;
+  out->max_gb_depth = c->gg.max_depth;
+  return RP_OK;
+}
+
+int rp_trace_open(rp_ctx* c, const char* path) {
+  if (!c || !path) return fail(RP_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->trace) std::fclose(c->trace);
+  c->trace = std::fopen(path, "w");
+  if (!c->trace) return fail(RP_EINVAL, std::string("cannot open trace file ") + path);
+  return RP_OK;
+}
+
+int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0, void* stream) {
+  std::string err;
+  const int rc = rp::launch_fill_xi(dst, n, seed, w, t, j0, stream, &err);
+  return rc == RP_OK ? rc : fail(rc, err);
+}
+
+}  // extern "C"

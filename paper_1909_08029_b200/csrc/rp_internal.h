@@ -1,0 +1,73 @@
+// Internal declarations of librp (not part of the ABI; see include/rp.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "rp.h"
+
+namespace rp {
+
+// ---- errors ------------------------------------------------------------------------
+// Sets the thread-local message returned by rp_last_error() and returns `code`.
+int fail(int code, const std::string& msg);
+
+// ---- static schedules (sched.cpp) ----------------------------------------------------
+// Fill group_of[w] (group index, -1 = skip) for `world` workers; returns RP_OK or RP_EINVAL.
+int schedule_paper4(int nodes, int m, int64_t step, int32_t* group_of, int32_t* n_groups);
+int schedule_shift_k(int n, int k, int64_t step, int32_t* group_of, int32_t* n_groups);
+
+// ---- Group Generator: Group Buffer + Global Division + filter (gg.cpp) ---------------
+constexpr int kGbCap = 4;        // Group Buffer depth bound (GD alone keeps depth <= 1)
+constexpr int kTableCap = 256;   // live groups
+
+struct GGGroup {
+  int64_t seq;     // -1 = free slot
+  int32_t size;
+  int32_t members[RP_MAX_GROUP];
+};
+
+// Plain-old-data so it can live in process-shared memory.
+struct GGState {
+  int32_t n, k, c_thres;
+  uint64_t rng;           // splitmix64 state
+  int64_t next_seq;
+  int32_t gb_len[RP_MAX_WORLD];
+  int64_t gb[RP_MAX_WORLD][kGbCap];
+  int64_t counters[RP_MAX_WORLD];
+  int64_t handed[RP_MAX_WORLD];   // seq handed to w by a request, -1 = none
+  uint64_t lock;
+  uint64_t retired, retiring;     // reading R19
+  GGGroup table[kTableCap];
+  int64_t gd_calls, requests, max_depth;
+};
+
+void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed);
+// Returns RP_OK and fills *out, or an RP_E* code.
+int gg_request(GGState* s, int w, rp_group* out);
+// Group `seq` completed: pop it from its members' GBs, clear lock bits.
+int gg_done(GGState* s, int64_t seq, rp_group* released);
+int gg_retire(GGState* s, int w);
+const GGGroup* gg_find(const GGState* s, int64_t seq);
+
+// ---- kernels (preduce.cu, xi.cu) -------------------------------------------------------
+// Several disjoint groups of EQUAL size k executed by one launch: members of
+// group gi are entries gi*k .. gi*k + k - 1 (group_first[gi] = gi*k), in
+// ascending worker id.
+constexpr int kMaxTasks = 16;
+constexpr int kMaxTaskMembers = 64;
+struct MultiTask {
+  int32_t ngroups;
+  int32_t group_k[kMaxTasks];
+  int32_t group_first[kMaxTasks];
+  float* x[kMaxTaskMembers];
+  const float* g[kMaxTaskMembers];   // nullptr: member has no staged step (y = x)
+  float lr[kMaxTaskMembers];
+};
+
+// Fused SGD + P-Reduce of groups whose members all live on the current GPU.
+int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::string* err);
+int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
+                   void* stream, std::string* err);
+
+}  // namespace rp

@@ -1,0 +1,359 @@
+"""ctypes binding of librp (include/rp.h). Argument marshalling only.
+
+Every C entry point has a same-named Python function here (``rp_init``,
+``rp_preduce``, ...). They raise :class:`RPError` on a non-zero status, with
+the library's thread-local message. :class:`Context` is a small convenience
+wrapper over the same calls. Device pointers are passed as integers
+(``tensor.data_ptr()``); streams as ``cudaStream_t`` integers
+(``torch.cuda.Stream.cuda_stream``).
+"""
+import ctypes
+import os
+
+RP_OK = 0
+RP_EINVAL = -1
+RP_ESTATE = -2
+RP_EPROTO = -3
+RP_ECONFLICT = -4
+RP_ETIMEOUT = -5
+RP_ECUDA = -6
+RP_ENOMEM = -7
+RP_ENODEV = -8
+
+RP_MAX_WORLD = 64
+RP_MAX_GROUP = 16
+RP_FLAG_TRACE = 0x1
+RP_FLAG_TIMING = 0x2
+RP_SCHED_PAPER4 = 1
+RP_SCHED_SHIFT_K = 2
+RP_WAIT_DEVICE = -1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def library_path():
+    return os.environ.get("RP_LIBRARY", os.path.join(_HERE, "librp.so"))
+
+
+class rp_config(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("n_gpus", ctypes.c_int32),
+        ("n_params", ctypes.c_int64),
+        ("workers_per_gpu", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("group_size", ctypes.c_int32),
+        ("c_thres", ctypes.c_int32),
+        ("nodes", ctypes.c_int32),
+        ("seed_gd", ctypes.c_uint64),
+        ("flags", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+class rp_group(ctypes.Structure):
+    _fields_ = [
+        ("seq", ctypes.c_int64),
+        ("size", ctypes.c_int32),
+        ("members", ctypes.c_int32 * RP_MAX_GROUP),
+    ]
+
+    def member_list(self):
+        return [int(self.members[i]) for i in range(self.size)]
+
+    @classmethod
+    def make(cls, seq, members):
+        g = cls()
+        g.seq = seq
+        g.size = len(members)
+        for i in range(RP_MAX_GROUP):
+            g.members[i] = members[i] if i < len(members) else -1
+        return g
+
+    def __repr__(self):
+        return f"rp_group(seq={self.seq}, members={self.member_list()})"
+
+
+class rp_stats(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "groups_launched", "singleton_groups", "cross_gpu_groups", "kernel_launches", "gd_calls",
+        "gg_requests", "max_gb_depth", "lock_assertions", "bytes_hbm", "bytes_nvlink")]
+
+    def as_dict(self):
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class rp_timing(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("total_ms", ctypes.c_double), ("min_ms", ctypes.c_double),
+                ("max_ms", ctypes.c_double), ("bytes_hbm", ctypes.c_int64), ("bytes_nvlink", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class RPError(RuntimeError):
+    def __init__(self, status, func, message):
+        super().__init__(f"{func} failed: status {status}: {message}")
+        self.status = status
+
+
+_P = ctypes.c_void_p
+_CTX = ctypes.c_void_p
+# name -> (restype, argtypes); the list is also what the ABI test checks against rp.h
+_SIGNATURES = {
+    "rp_init": (ctypes.c_int, [ctypes.POINTER(rp_config), ctypes.POINTER(_CTX)]),
+    "rp_finalize": (ctypes.c_int, [_CTX]),
+    "rp_bind_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, _P]),
+    "rp_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(_P)]),
+    "rp_set_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, _P]),
+    "rp_schedule_static": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64,
+                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "rp_schedule_static_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                                 ctypes.POINTER(rp_group)]),
+    "rp_group_generate": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(rp_group)]),
+    "rp_gg_release": (ctypes.c_int, [_CTX, ctypes.c_int64]),
+    "rp_retire": (ctypes.c_int, [_CTX, ctypes.c_int32]),
+    "rp_step": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float]),
+    "rp_preduce": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(rp_group)]),
+    "rp_barrier_free_wait": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64]),
+    "rp_batch_begin": (ctypes.c_int, [_CTX]),
+    "rp_batch_end": (ctypes.c_int, [_CTX]),
+    "rp_timing_read": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_timing)]),
+    "rp_stats_get": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_stats)]),
+    "rp_trace_open": (ctypes.c_int, [_CTX, ctypes.c_char_p]),
+    "rp_last_error": (ctypes.c_char_p, []),
+    "rp_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "rp_abi_version": (ctypes.c_int, []),
+    "rp_fill_xi": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                  ctypes.c_uint64, _P]),
+}
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+lib = None
+
+
+def load_library(path=None):
+    """Load librp.so (raises OSError if it was not built: there is no fallback)."""
+    global lib
+    if lib is not None and path is None:
+        return lib
+    p = path or library_path()
+    if not os.path.exists(p):
+        raise OSError(f"librp.so not found at {p}: run `make -C paper_1909_08029_b200` "
+                      "or __graft_entry__.build(); there is no CPU fallback")
+    handle = ctypes.CDLL(p)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    if handle.rp_abi_version() != 1:
+        raise OSError("librp ABI version mismatch")
+    lib = handle
+    return lib
+
+
+def _check(status, func):
+    if status != RP_OK:
+        msg = load_library().rp_last_error()
+        raise RPError(status, func, (msg or b"").decode(errors="replace"))
+    return status
+
+
+def _ptr(v):
+    if v is None:
+        return None
+    if hasattr(v, "data_ptr"):
+        return ctypes.c_void_p(v.data_ptr())
+    return ctypes.c_void_p(int(v))
+
+
+# ---- same-named functions ----------------------------------------------------------
+
+def rp_init(cfg):
+    L = load_library()
+    out = _CTX()
+    _check(L.rp_init(ctypes.byref(cfg), ctypes.byref(out)), "rp_init")
+    return out
+
+
+def rp_finalize(ctx):
+    _check(load_library().rp_finalize(ctx), "rp_finalize")
+
+
+def rp_bind_worker(ctx, w, x, g=None):
+    _check(load_library().rp_bind_worker(ctx, w, _ptr(x), _ptr(g)), "rp_bind_worker")
+
+
+def rp_worker_stream(ctx, w):
+    out = _P()
+    _check(load_library().rp_worker_stream(ctx, w, ctypes.byref(out)), "rp_worker_stream")
+    return out.value or 0
+
+
+def rp_set_worker_stream(ctx, w, stream):
+    _check(load_library().rp_set_worker_stream(ctx, w, _ptr(stream)), "rp_set_worker_stream")
+
+
+def rp_schedule_static(ctx, rule, step, world):
+    arr = (ctypes.c_int32 * world)()
+    ng = ctypes.c_int32()
+    _check(load_library().rp_schedule_static(ctx, rule, step, arr, ctypes.byref(ng)), "rp_schedule_static")
+    return [int(v) for v in arr], int(ng.value)
+
+
+def rp_schedule_static_worker(ctx, rule, step, w):
+    g = rp_group()
+    _check(load_library().rp_schedule_static_worker(ctx, rule, step, w, ctypes.byref(g)),
+           "rp_schedule_static_worker")
+    return g
+
+
+def rp_group_generate(ctx, w):
+    g = rp_group()
+    _check(load_library().rp_group_generate(ctx, w, ctypes.byref(g)), "rp_group_generate")
+    return g
+
+
+def rp_gg_release(ctx, seq):
+    _check(load_library().rp_gg_release(ctx, seq), "rp_gg_release")
+
+
+def rp_retire(ctx, w):
+    _check(load_library().rp_retire(ctx, w), "rp_retire")
+
+
+def rp_step(ctx, w, grad, lr):
+    _check(load_library().rp_step(ctx, w, _ptr(grad), ctypes.c_float(lr)), "rp_step")
+
+
+def rp_preduce(ctx, w, group):
+    _check(load_library().rp_preduce(ctx, w, ctypes.byref(group)), "rp_preduce")
+
+
+def rp_barrier_free_wait(ctx, w, timeout_us):
+    _check(load_library().rp_barrier_free_wait(ctx, w, timeout_us), "rp_barrier_free_wait")
+
+
+def rp_batch_begin(ctx):
+    _check(load_library().rp_batch_begin(ctx), "rp_batch_begin")
+
+
+def rp_batch_end(ctx):
+    _check(load_library().rp_batch_end(ctx), "rp_batch_end")
+
+
+def rp_timing_read(ctx):
+    t = rp_timing()
+    _check(load_library().rp_timing_read(ctx, ctypes.byref(t)), "rp_timing_read")
+    return t.as_dict()
+
+
+def rp_stats_get(ctx):
+    s = rp_stats()
+    _check(load_library().rp_stats_get(ctx, ctypes.byref(s)), "rp_stats_get")
+    return s.as_dict()
+
+
+def rp_trace_open(ctx, path):
+    _check(load_library().rp_trace_open(ctx, str(path).encode()), "rp_trace_open")
+
+
+def rp_fill_xi(dst, n, seed, w, t, j0=0, stream=0):
+    _check(load_library().rp_fill_xi(_ptr(dst), n, seed, w, t, j0, _ptr(stream)), "rp_fill_xi")
+
+
+fill_xi = rp_fill_xi
+
+
+class Context:
+    """Owns one rp_ctx. Methods map 1:1 onto the C calls."""
+
+    def __init__(self, world, n_params, *, n_gpus=1, workers_per_gpu=None, rank=0, device=None,
+                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0):
+        cfg = rp_config()
+        cfg.world = world
+        cfg.n_gpus = n_gpus
+        cfg.n_params = n_params
+        cfg.workers_per_gpu = workers_per_gpu if workers_per_gpu else (world // n_gpus if n_gpus else world)
+        cfg.rank = rank
+        cfg.device = rank if device is None else device
+        cfg.group_size = group_size
+        cfg.c_thres = c_thres
+        cfg.nodes = nodes
+        cfg.seed_gd = seed_gd
+        cfg.flags = flags
+        self.cfg = cfg
+        self.world = world
+        self.n_params = n_params
+        self.wpg = cfg.workers_per_gpu
+        self.rank = rank
+        self.handle = rp_init(cfg)
+
+    def local_workers(self):
+        return list(range(self.rank * self.wpg, (self.rank + 1) * self.wpg))
+
+    def close(self):
+        if self.handle:
+            rp_finalize(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bind_worker(self, w, x, g=None):
+        rp_bind_worker(self.handle, w, x, g)
+
+    def worker_stream(self, w):
+        return rp_worker_stream(self.handle, w)
+
+    def set_worker_stream(self, w, stream):
+        rp_set_worker_stream(self.handle, w, stream)
+
+    def schedule_static(self, rule, step):
+        return rp_schedule_static(self.handle, rule, step, self.world)
+
+    def schedule_static_worker(self, rule, step, w):
+        return rp_schedule_static_worker(self.handle, rule, step, w)
+
+    def group_generate(self, w):
+        return rp_group_generate(self.handle, w)
+
+    def gg_release(self, seq):
+        rp_gg_release(self.handle, seq)
+
+    def retire(self, w):
+        rp_retire(self.handle, w)
+
+    def step(self, w, grad=None, lr=0.1):
+        rp_step(self.handle, w, grad, lr)
+
+    def preduce(self, w, group):
+        rp_preduce(self.handle, w, group)
+
+    def barrier_free_wait(self, w, timeout_us=RP_WAIT_DEVICE):
+        rp_barrier_free_wait(self.handle, w, timeout_us)
+
+    def batch_begin(self):
+        rp_batch_begin(self.handle)
+
+    def batch_end(self):
+        rp_batch_end(self.handle)
+
+    def timing_read(self):
+        return rp_timing_read(self.handle)
+
+    def stats(self):
+        return rp_stats_get(self.handle)
+
+    def trace_open(self, path):
+        rp_trace_open(self.handle, path)

@@ -1,0 +1,136 @@
+"""Lockstep driver of one GPU's workers through the public librp API.
+
+One call of :meth:`LockstepRunner.step` is one training iteration of alg1
+ for every local worker, in the engine's fast path:
+
+  Step 2  synthetic gradient on the worker's stream (rp_fill_xi) + rp_step
+  Step 3  rp_schedule_static_worker or rp_group_generate for every
+          worker in ascending order (GB + GD; every rank runs the
+          same deterministic GG)
+  Step 4  rp_batch_begin / rp_preduce per local worker / rp_batch_end
+          (all of this GPU's groups in one fused kernel launch)
+  wait    rp_barrier_free_wait(RP_WAIT_DEVICE): stream-ordered, no host block
+
+PyTorch supplies device memory only. Replicas are rows of one (wpg, ld)
+fp32 tensor with a 64-element-aligned row stride ld (16-B aligned rows for
+any n_params), gradients likewise.
+"""
+import torch
+
+from . import rp
+from .rp import Context, RP_SCHED_PAPER4, RP_SCHED_SHIFT_K, RP_WAIT_DEVICE
+
+SEED_X = 1   # x_w^0[j] = xi(1, w, 0, j)
+SEED_G = 2   #                            g_w^t[j] = xi(2, w, t, j)
+
+RULES = {"paper4": RP_SCHED_PAPER4, "shift_k": RP_SCHED_SHIFT_K}
+
+
+def _ceil_to(v, m):
+    return (v + m - 1) // m * m
+
+
+class LockstepRunner:
+    def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
+                 lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True):
+        if mode not in ("static", "gd"):
+            raise ValueError("mode must be 'static' or 'gd'")
+        if mode == "static" and rule not in RULES:
+            raise ValueError("static mode needs rule 'paper4' or 'shift_k'")
+        if grad_mode not in ("per_step", "resident"):
+            raise ValueError("grad_mode must be 'per_step' or 'resident'")
+        self.device = rank if device is None else device
+        torch.cuda.set_device(self.device)
+        self.mode, self.rule, self.lr, self.grad_mode = mode, rule, lr, grad_mode
+        self.world, self.n = world, n_params
+        self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device,
+                           group_size=group_size, c_thres=c_thres, nodes=nodes, seed_gd=seed_gd, flags=flags)
+        self.local = self.ctx.local_workers()
+        self.ld = _ceil_to(n_params, 64)
+        dev = torch.device("cuda", self.device)
+        self.X = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
+        self.G = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
+        self.streams = {}
+        for i, w in enumerate(self.local):
+            self.ctx.bind_worker(w, self.x(w), self.g(w))
+            self.streams[w] = self.ctx.worker_stream(w)
+        self.t = 0
+        if init:
+            self.init_replicas()
+        if grad_mode == "resident":
+            for w in self.local:
+                rp.fill_xi(self.g(w), n_params, SEED_G, w, 1, 0, self.streams[w])
+        self.synchronize()
+
+    # -- memory ----------------------------------------------------------------------
+    def _row(self, w):
+        return self.local.index(w)
+
+    def x(self, w):
+        return self.X[self._row(w), :self.n]
+
+    def g(self, w):
+        return self.G[self._row(w), :self.n]
+
+    def init_replicas(self):
+        for w in self.local:
+            rp.fill_xi(self.x(w), self.n, SEED_X, w, 0, 0, self.streams[w])
+        self.t = 0
+
+    def synchronize(self):
+        torch.cuda.synchronize(self.device)
+
+    # -- one lockstep step ---------------------------------------------------------------
+    def groups_for_step(self, t):
+        """Step 3 for every local worker; returns ({w: rp_group}, [seq of non-local GG groups])."""
+        groups, foreign = {}, []
+        if self.mode == "static":
+            for w in self.local:
+                groups[w] = self.ctx.schedule_static_worker(RULES[self.rule], t, w)
+        else:
+            local = set(self.local)
+            seen = set()
+            for w in range(self.world):           # same request order on every rank
+                g = self.ctx.group_generate(w)
+                if w in local:
+                    groups[w] = g
+                elif g.seq not in seen and not (set(g.member_list()) & local):
+                    foreign.append(g.seq)
+                seen.add(g.seq)
+            foreign = sorted(set(foreign))
+        return groups, foreign
+
+    def step(self, grads=None):
+        """One lockstep step; `grads` optionally maps w -> device tensor to use as g."""
+        t = self.t + 1
+        for w in self.local:
+            if grads is not None:
+                self.ctx.step(w, grads[w], self.lr)
+            else:
+                if self.grad_mode == "per_step":
+                    rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, self.streams[w])
+                self.ctx.step(w, None, self.lr)
+        groups, foreign = self.groups_for_step(t)
+        self.ctx.batch_begin()
+        try:
+            for w in self.local:
+                self.ctx.preduce(w, groups[w])
+        finally:
+            self.ctx.batch_end()
+        for w in self.local:
+            self.ctx.barrier_free_wait(w, RP_WAIT_DEVICE)
+        for seq in foreign:
+            self.ctx.gg_release(seq)
+        self.t = t
+        return groups
+
+    def run(self, steps):
+        log = []
+        for _ in range(steps):
+            groups = self.step()
+            log.append((self.t, sorted({tuple(g.member_list()) for g in groups.values()})))
+        return log
+
+    def close(self):
+        self.synchronize()
+        self.ctx.close()
