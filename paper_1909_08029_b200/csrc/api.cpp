@@ -69,6 +69,7 @@ struct ActiveGroup {
   uint64_t arrived = 0;
   uint64_t waited = 0;
   bool launched = false;
+  bool released = false;  // GG release done (first observed completion)
   const float* grad[RP_MAX_GROUP] = {};
   float lr[RP_MAX_GROUP] = {};
 };
@@ -200,51 +201,47 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& seqs) {
   WorkerSlot& L = c->w[launcher];
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if (((all >> m) & 1) && m != launcher) CUDA_TRY(cudaStreamWaitEvent(L.stream, c->w[m].ev_arrive, 0));
-  // One launch per distinct group size (kernels are specialized on k); each
-  // launch packs up to kMaxTasks groups / kMaxTaskMembers members.
-  std::map<int, std::vector<int64_t>> by_size;
-  for (int64_t q : seqs) by_size[c->active.at(q).g.size].push_back(q);
-  for (auto& kv : by_size) {
-    const std::vector<int64_t>& list = kv.second;
-    size_t gi = 0;
-    while (gi < list.size()) {
-      rp::MultiTask t{};
-      int nm = 0;
-      int64_t bytes = 0;
-      while (gi < list.size() && t.ngroups < rp::kMaxTasks && nm + kv.first <= rp::kMaxTaskMembers) {
-        ActiveGroup& a = c->active.at(list[gi]);
-        t.group_k[t.ngroups] = a.g.size;
-        t.group_first[t.ngroups] = nm;
-        for (int i = 0; i < a.g.size; ++i) {
-          t.x[nm] = c->w[a.g.members[i]].x;
-          t.g[nm] = a.grad[i];
-          t.lr[nm] = a.lr[i];
-          bytes += (a.grad[i] ? 12 : 8) * c->cfg.n_params;
-          ++nm;
-        }
-        t.ngroups++;
-        if (a.g.size == 1) c->stats.singleton_groups++;
-        c->stats.groups_launched++;
-        ++gi;
+  // One fused launch for all ready groups (chunked at kMaxTasks groups /
+  // kMaxTaskMembers members).
+  size_t gi = 0;
+  while (gi < seqs.size()) {
+    rp::MultiTask t{};
+    int nm = 0;
+    int64_t bytes = 0;
+    while (gi < seqs.size() && t.ngroups < rp::kMaxTasks) {
+      ActiveGroup& a = c->active.at(seqs[gi]);
+      if (nm + a.g.size > rp::kMaxTaskMembers) break;
+      t.group_k[t.ngroups] = a.g.size;
+      t.group_first[t.ngroups] = nm;
+      for (int i = 0; i < a.g.size; ++i) {
+        t.x[nm] = c->w[a.g.members[i]].x;
+        t.g[nm] = a.grad[i];
+        t.lr[nm] = a.lr[i];
+        bytes += (a.grad[i] ? 12 : 8) * c->cfg.n_params;
+        ++nm;
       }
-      const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (timing) {
-        e0 = timing_event(c);
-        e1 = timing_event(c);
-        if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
-        CUDA_TRY(cudaEventRecord(e0, L.stream));
-      }
-      std::string err;
-      const int rc = rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
-      if (rc != RP_OK) return fail(rc, err);
-      if (timing) {
-        CUDA_TRY(cudaEventRecord(e1, L.stream));
-        c->timed.push_back({e0, e1, bytes, 0});
-      }
-      c->stats.kernel_launches++;
-      c->stats.bytes_hbm += bytes;
+      t.ngroups++;
+      if (a.g.size == 1) c->stats.singleton_groups++;
+      c->stats.groups_launched++;
+      ++gi;
     }
+    const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+      e0 = timing_event(c);
+      e1 = timing_event(c);
+      if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
+      CUDA_TRY(cudaEventRecord(e0, L.stream));
+    }
+    std::string err;
+    const int rc = rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
+    if (rc != RP_OK) return fail(rc, err);
+    if (timing) {
+      CUDA_TRY(cudaEventRecord(e1, L.stream));
+      c->timed.push_back({e0, e1, bytes, 0});
+    }
+    c->stats.kernel_launches++;
+    c->stats.bytes_hbm += bytes;
   }
   CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
   for (int m = 0; m < RP_MAX_WORLD; ++m) {
@@ -573,12 +570,16 @@ int rp_barrier_free_wait(rp_ctx* c, int32_t w, int64_t timeout_us) {
   s.in_group = false;
   c->inflight &= ~(1ull << w);
   a.waited |= 1ull << w;
-  if ((a.waited & a.local_mask) == a.local_mask) {
-    const bool gg_group = seq >= 0;
-    c->active.erase(seq);
-    if (gg_group) return release_gg_group(c, seq);
+  // Reading R11: the GG releases the group at the first observation of its
+  // completion (host-observed, or stream-ordered for RP_WAIT_DEVICE), so the
+  // members' Group Buffers advance even if some member has not waited yet.
+  int rc = RP_OK;
+  if (!a.released) {
+    a.released = true;
+    if (seq >= 0) rc = release_gg_group(c, seq);
   }
-  return RP_OK;
+  if ((a.waited & a.local_mask) == a.local_mask) c->active.erase(seq);
+  return rc;
 }
 
 int rp_batch_begin(rp_ctx* c) {

@@ -6,8 +6,8 @@
 //   x_m[j] = xbar                              for m in G
 // y is never stored. Non-members are not touched (F^G_uu = 1).
 // One launch executes several disjoint groups at once ("non-conflicting
-// F^G's can be executed concurrently"): the element range of every
-// group is cut into tiles and the persistent grid walks the union of tiles.
+// F^G's can be executed concurrently"): the resident grid is shared
+// out among the groups in proportion to their bytes.
 //
 // Pinned fp32 arithmetic (reading R1): __fmul_rn / __fsub_rn /
 // __fadd_rn / __fdiv_rn (no FMA contraction), left fold over members in
@@ -62,17 +62,17 @@ __device__ __forceinline__ float fold_mean(const float (&y)[K]) {
   return K == 1 ? s : __fdiv_rn(s, static_cast<float>(K));
 }
 
-// One tile of group gi: float4 indices [i0, i0 + kThreads*U) of every member.
+// One tile of the group whose members start at `first`: float4 indices [i0, i0 + kThreads*U) of every member.
 template <int K, int U>
-__device__ __forceinline__ void group_tile(const MultiTask& t, int gi, int64_t i0, int64_t n4) {
+__device__ __forceinline__ void group_tile(const MultiTask& t, int first, int64_t i0, int64_t n4) {
   float* x[K];
   const float* g[K];
   float lr[K];
 #pragma unroll
   for (int m = 0; m < K; ++m) {
-    x[m] = t.x[gi * K + m];
-    g[m] = t.g[gi * K + m];
-    lr[m] = t.lr[gi * K + m];
+    x[m] = t.x[first + m];
+    g[m] = t.g[first + m];
+    lr[m] = t.lr[first + m];
   }
   float4 xv[U][K], gv[U][K];
 #pragma unroll
@@ -112,44 +112,74 @@ __device__ __forceinline__ void group_tile(const MultiTask& t, int gi, int64_t i
   }
 }
 
-// Element j of group gi, scalar (the n mod 4 ragged tail).
+// Element j of the group whose members start at `first`, scalar (the n mod 4 tail).
 template <int K>
-__device__ __forceinline__ void group_scalar(const MultiTask& t, int gi, int64_t j) {
+__device__ __forceinline__ void group_scalar(const MultiTask& t, int first, int64_t j) {
   float y[K];
 #pragma unroll
   for (int m = 0; m < K; ++m) {
-    const float* g = t.g[gi * K + m];
-    const float xj = t.x[gi * K + m][j];
-    y[m] = g != nullptr ? sgd(xj, g[j], t.lr[gi * K + m]) : xj;
+    const float* g = t.g[first + m];
+    const float xj = t.x[first + m][j];
+    y[m] = g != nullptr ? sgd(xj, g[j], t.lr[first + m]) : xj;
   }
   const float r = fold_mean<K>(y);
 #pragma unroll
-  for (int m = 0; m < K; ++m) t.x[gi * K + m][j] = r;
+  for (int m = 0; m < K; ++m) t.x[first + m][j] = r;
 }
 
-// All t.ngroups groups have exactly K members (the engine splits a batch by
-// group size, so each instantiation keeps the register budget of its K).
-// Persistent grid over ngroups * tiles tiles, groups interleaved tile by tile.
+// CTA blocks [cta_begin[gi], cta_begin[gi+1]) work on group gi only (CTAs are
+// shared out in proportion to each group's bytes), so a CTA runs a single
+// K-specialized loop for its whole life. Each CTA grid-strides over its group's
+// tiles.
 template <int K, int U>
+__device__ __forceinline__ void group_loop(const MultiTask& t, int gi, int first, int64_t n4, int64_t n) {
+  const int64_t nb = t.cta_begin[gi + 1] - t.cta_begin[gi];
+  const int64_t b = static_cast<int64_t>(blockIdx.x) - t.cta_begin[gi];
+  const int64_t tiles = (n4 + kThreads * U - 1) / (kThreads * U);
+  for (int64_t tile = b; tile < tiles; tile += nb) group_tile<K, U>(t, first, tile * kThreads * U, n4);
+  const int64_t rem = n - 4 * n4;  // ragged tail: first CTA of the group, scalar
+  if (b == 0 && threadIdx.x < rem) group_scalar<K>(t, first, 4 * n4 + threadIdx.x);
+}
+
+template <int K, int U, int KMAX>
+__device__ __forceinline__ void loop_if(const MultiTask& t, int gi, int first, int64_t n4, int64_t n) {
+  if constexpr (K <= KMAX) group_loop<K, U>(t, gi, first, n4, n);
+}
+
+// KMAX bounds the instantiated group sizes (and so the register budget).
+template <int KMAX, int U>
 __global__ void __launch_bounds__(kThreads) preduce_multi_kernel(const MultiTask t, const int64_t n4,
-                                                                const int64_t n, const int64_t tiles) {
-  const int64_t total = tiles * t.ngroups;
-  for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
-    const int gi = static_cast<int>(q % t.ngroups);
-    group_tile<K, U>(t, gi, (q / t.ngroups) * kThreads * U, n4);
+                                                                const int64_t n) {
+  int gi = 0;
+  while (gi + 1 < t.ngroups && static_cast<int>(blockIdx.x) >= t.cta_begin[gi + 1]) ++gi;
+  const int first = t.group_first[gi];
+  switch (t.group_k[gi]) {
+    case 1: loop_if<1, U, KMAX>(t, gi, first, n4, n); break;
+    case 2: loop_if<2, U, KMAX>(t, gi, first, n4, n); break;
+    case 3: loop_if<3, U, KMAX>(t, gi, first, n4, n); break;
+    case 4: loop_if<4, U, KMAX>(t, gi, first, n4, n); break;
+    case 5: loop_if<5, U, KMAX>(t, gi, first, n4, n); break;
+    case 6: loop_if<6, U, KMAX>(t, gi, first, n4, n); break;
+    case 7: loop_if<7, U, KMAX>(t, gi, first, n4, n); break;
+    case 8: loop_if<8, U, KMAX>(t, gi, first, n4, n); break;
+    case 9: loop_if<9, U, KMAX>(t, gi, first, n4, n); break;
+    case 10: loop_if<10, U, KMAX>(t, gi, first, n4, n); break;
+    case 11: loop_if<11, U, KMAX>(t, gi, first, n4, n); break;
+    case 12: loop_if<12, U, KMAX>(t, gi, first, n4, n); break;
+    case 13: loop_if<13, U, KMAX>(t, gi, first, n4, n); break;
+    case 14: loop_if<14, U, KMAX>(t, gi, first, n4, n); break;
+    case 15: loop_if<15, U, KMAX>(t, gi, first, n4, n); break;
+    default: loop_if<16, U, KMAX>(t, gi, first, n4, n); break;
   }
-  const int64_t rem = n - 4 * n4;
-  if (blockIdx.x == 0 && threadIdx.x < rem * t.ngroups)
-    group_scalar<K>(t, static_cast<int>(threadIdx.x / rem), 4 * n4 + threadIdx.x % rem);
 }
 
 int g_num_sms = 0;
 
-template <int K, int U>
-int launch_k(const MultiTask& t, int64_t n, cudaStream_t stream, std::string* err) {
+template <int KMAX, int U>
+int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
   static int occ = 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<K, U>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<KMAX, U>, kThreads, 0) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
@@ -161,11 +191,20 @@ int launch_k(const MultiTask& t, int64_t n, cudaStream_t stream, std::string* er
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   const int64_t n4 = n / 4;
-  const int64_t tiles = (n4 + kThreads * U - 1) / (kThreads * U);
-  const int64_t want = std::max<int64_t>(1, tiles * t.ngroups);
-  const int64_t cap = static_cast<int64_t>(g_num_sms) * occ;
-  const int blocks = static_cast<int>(std::min(want, cap));
-  preduce_multi_kernel<K, U><<<blocks, kThreads, 0, stream>>>(t, n4, n, tiles);
+  const int64_t tiles = std::max<int64_t>(1, (n4 + kThreads * U - 1) / (kThreads * U));
+  // CTAs in proportion to each group's bytes (k members), at least one, at most its tile count
+  int64_t kt = 0;
+  for (int gi = 0; gi < t.ngroups; ++gi) kt += t.group_k[gi];
+  const int64_t cap = std::max<int64_t>(static_cast<int64_t>(g_num_sms) * occ, t.ngroups);
+  int32_t acc = 0;
+  for (int gi = 0; gi < t.ngroups; ++gi) {
+    t.cta_begin[gi] = acc;
+    int64_t share = (cap * t.group_k[gi]) / kt;
+    share = std::max<int64_t>(1, std::min(share, tiles));
+    acc += static_cast<int32_t>(share);
+  }
+  t.cta_begin[t.ngroups] = acc;
+  preduce_multi_kernel<KMAX, U><<<acc, kThreads, 0, stream>>>(t, n4, n);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("preduce kernel launch: ") + cudaGetErrorString(e);
@@ -181,42 +220,27 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     *err = "preduce: bad group count";
     return RP_EINVAL;
   }
-  const int k = t.group_k[0];
-  if (k < 1 || k > RP_MAX_GROUP || k * t.ngroups > kMaxTaskMembers) {
-    *err = "preduce: bad group size";
-    return RP_EINVAL;
-  }
+  int kmax = 0, nm = 0;
   for (int gi = 0; gi < t.ngroups; ++gi) {
-    if (t.group_k[gi] != k || t.group_first[gi] != gi * k) {
-      *err = "preduce: groups of one launch must have equal size and packed members";
+    const int k = t.group_k[gi];
+    if (k < 1 || k > RP_MAX_GROUP || t.group_first[gi] != nm || nm + k > kMaxTaskMembers) {
+      *err = "preduce: bad group descriptor";
       return RP_EINVAL;
     }
+    nm += k;
+    kmax = std::max(kmax, k);
   }
-  for (int i = 0; i < k * t.ngroups; ++i) {
+  for (int i = 0; i < nm; ++i) {
     if (!t.x[i] || (reinterpret_cast<uintptr_t>(t.x[i]) & 15) || (reinterpret_cast<uintptr_t>(t.g[i]) & 15)) {
       *err = "preduce: replica and gradient pointers must be non-null and 16-byte aligned";
       return RP_EINVAL;
     }
   }
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (k) {
-    case 1: return launch_k<1, 4>(t, n, s, err);
-    case 2: return launch_k<2, 2>(t, n, s, err);
-    case 3: return launch_k<3, 2>(t, n, s, err);
-    case 4: return launch_k<4, 2>(t, n, s, err);
-    case 5: return launch_k<5, 1>(t, n, s, err);
-    case 6: return launch_k<6, 1>(t, n, s, err);
-    case 7: return launch_k<7, 1>(t, n, s, err);
-    case 8: return launch_k<8, 1>(t, n, s, err);
-    case 9: return launch_k<9, 1>(t, n, s, err);
-    case 10: return launch_k<10, 1>(t, n, s, err);
-    case 11: return launch_k<11, 1>(t, n, s, err);
-    case 12: return launch_k<12, 1>(t, n, s, err);
-    case 13: return launch_k<13, 1>(t, n, s, err);
-    case 14: return launch_k<14, 1>(t, n, s, err);
-    case 15: return launch_k<15, 1>(t, n, s, err);
-    default: return launch_k<16, 1>(t, n, s, err);
-  }
+  if (kmax <= 2) return launch_kmax<2, 2>(t, n, s, err);
+  if (kmax <= 4) return launch_kmax<4, 2>(t, n, s, err);
+  if (kmax <= 8) return launch_kmax<8, 1>(t, n, s, err);
+  return launch_kmax<16, 1>(t, n, s, err);
 }
 
 }  // namespace rp

@@ -51,9 +51,9 @@ int gg_retire(GGState* s, int w);
 const GGGroup* gg_find(const GGState* s, int64_t seq);
 
 // ---- kernels (preduce.cu, xi.cu) -------------------------------------------------------
-// Several disjoint groups of EQUAL size k executed by one launch: members of
-// group gi are entries gi*k .. gi*k + k - 1 (group_first[gi] = gi*k), in
-// ascending worker id.
+// Several disjoint groups executed by one launch: members of group gi are
+// entries group_first[gi] .. group_first[gi] + group_k[gi] - 1 (packed, in
+// ascending worker id). cta_begin is filled by the launcher.
 constexpr int kMaxTasks = 16;
 constexpr int kMaxTaskMembers = 64;
 struct MultiTask {
@@ -63,6 +63,7 @@ struct MultiTask {
   float* x[kMaxTaskMembers];
   const float* g[kMaxTaskMembers];   // nullptr: member has no staged step (y = x)
   float lr[kMaxTaskMembers];
+  int32_t cta_begin[kMaxTasks + 1];
 };
 
 // Fused SGD + P-Reduce of groups whose members all live on the current GPU.

@@ -85,7 +85,7 @@ def test_mixed_group_sizes_in_one_batch():
         ctx.barrier_free_wait(w, rp.RP_WAIT_DEVICE)
     torch.cuda.synchronize()
     st = ctx.stats()
-    assert st["kernel_launches"] == 3                   # one per distinct size (3, 2, 1)
+    assert st["kernel_launches"] == 1                   # all sizes (3, 3, 2, 1, 3) in one launch
     assert st["groups_launched"] == 5 and st["singleton_groups"] == 1
     assert st["bytes_hbm"] == 12 * world * n
     for g in groups:
@@ -112,4 +112,27 @@ def test_explicit_gradient_pointer_and_lr_per_member():
           2: U.sgd_fp32(Xh[2], None, F32(0))}
     want = U.preduce_fp32(ys, [0, 1, 2])
     assert np.array_equal(X[2, :n].cpu().numpy(), want)
+    ctx.close()
+
+
+def test_more_groups_than_one_launch_holds():
+    world, n = 40, 4099                                 # 20 pairs -> 16 + 4 groups, two launches
+    ctx, X, G = _setup(world, n)
+    Xh = {w: X[w, :n].cpu().numpy().copy() for w in range(world)}
+    Gh = {w: G[w, :n].cpu().numpy().copy() for w in range(world)}
+    ctx.batch_begin()
+    for p in range(20):
+        grp = rp.rp_group.make(-(p + 1), [2 * p, 2 * p + 1])
+        for m in grp.member_list():
+            ctx.step(m, None, 0.1)
+            ctx.preduce(m, grp)
+    ctx.batch_end()
+    for w in range(world):
+        ctx.barrier_free_wait(w, rp.RP_WAIT_DEVICE)
+    torch.cuda.synchronize()
+    assert ctx.stats()["kernel_launches"] == 2
+    for p in range(20):
+        U.fused_group_update(Xh, {m: Gh[m] for m in (2 * p, 2 * p + 1)}, [2 * p, 2 * p + 1], F32(0.1))
+    for w in range(world):
+        assert np.array_equal(X[w, :n].cpu().numpy(), Xh[w])
     ctx.close()
