@@ -33,9 +33,18 @@ L2_BYTES = 126 * 2**20
 WORKLOADS = {
     "cfg1": dict(desc="configs[0]: 4 workers, 1M fp32, k=2, static SHIFT_K(4,2), 1 GPU",
                  wpg=4, n=1 << 20, k=2, mode="static", rule="shift_k"),
-    "cfg2": dict(desc="configs[1]: 8 workers on 1 B200, ResNet-50-sized 25.6M fp32, k=3, GB+GD",
+    "cfg2": dict(desc="configs[1]: 8 workers per B200, ResNet-50-sized 25.6M fp32, k=3, GB+GD over all "
+                      "8*N workers (N=1: exactly configs[1]; N>1: weak scaling of that layout)",
                  wpg=8, n=N_R50, k=3, mode="gd", rule=None),
+    "cfg3": dict(desc="configs[2]: 1 worker per B200 (8 workers on 8 GPUs), ResNet-50-sized, k=3, GB+GD, "
+                      "concurrent disjoint groups over NVLink",
+                 wpg=1, n=N_R50, k=3, mode="gd", rule=None),
+    "cfg4": dict(desc="configs[3]: 2 workers per B200 (16 on 8 GPUs), VGG-16-sized 138M fp32, k=3, static "
+                      "SHIFT_K(2N,3)",
+                 wpg=2, n=N_VGG, k=3, mode="static", rule="shift_k"),
 }
+NVLINK_PEAK = 770.0   # GB/s per direction, measured peer copy (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0
 
 
 def measured_peaks():
@@ -113,19 +122,54 @@ def init_dist(args):
 # ours
 # ------------------------------------------------------------------------------------------
 
+def setup_dist(n_gpus, local_rank):
+    """NCCL default group (plumbing + the NCCL baseline) and a gloo group for host metadata."""
+    import torch
+    import torch.distributed as dist
+    if n_gpus == 1:
+        return None
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    return dist.new_group(backend="gloo")
+
+
+def max_over_ranks(v, pg):
+    import torch
+    import torch.distributed as dist
+    if pg is None:
+        return v
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
+    return float(t.item())
+
+
+def gather(obj, pg):
+    import torch.distributed as dist
+    if pg is None:
+        return [obj]
+    out = [None] * dist.get_world_size(pg)
+    dist.all_gather_object(out, obj, group=pg)
+    return out
+
+
+def barrier(pg):
+    import torch.distributed as dist
+    if pg is not None:
+        dist.barrier(group=pg)
+
+
 def run_ours(args, wl):
     import torch
     import paper_1909_08029_b200 as rp
     from paper_1909_08029_b200.runner import LockstepRunner
 
     rank, local_rank, n_gpus = init_dist(args)
-    if n_gpus > 1:
-        raise SystemExit("multi-GPU bench not wired yet")
     torch.cuda.set_device(local_rank)
+    pg = setup_dist(n_gpus, local_rank)
     wpg, n, k = wl["wpg"], wl["n"], wl["k"]
     world = wpg * n_gpus
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
-                            rank=rank, device=local_rank, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
+                            rank=rank, device=local_rank, grad_mode="resident", flags=rp.RP_FLAG_TIMING,
+                            peer_group=pg)
     for _ in range(args.warmup):
         runner.step()
     runner.synchronize()
@@ -133,6 +177,7 @@ def run_ours(args, wl):
     s0 = torch.cuda.ExternalStream(runner.streams[runner.local[0]])   # every batch launches here
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st0 = runner.ctx.stats()
+    barrier(pg)
     with ClockSampler(local_rank) as clk:
         runner.synchronize()
         ev0.record(s0)
@@ -140,16 +185,55 @@ def run_ours(args, wl):
             runner.step()
         ev1.record(s0)
         runner.synchronize()
+    barrier(pg)
     st1 = runner.ctx.stats()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), pg)
     tim = runner.ctx.timing_read()
-    bytes_step = (st1["bytes_hbm"] - st0["bytes_hbm"]) / args.steps
     launches = st1["kernel_launches"] - st0["kernel_launches"]
+    per_rank = gather({"tim": tim, "launches": launches, "clocks": clk.summary(),
+                       "hbm": st1["bytes_hbm"] - st0["bytes_hbm"],
+                       "nvl": st1["bytes_nvlink"] - st0["bytes_nvlink"],
+                       "cross": st1["cross_gpu_groups"] - st0["cross_gpu_groups"]}, pg)
+    e2e = run_e2e(runner, args, torch, pg)
+    runner.close()
+    if rank != 0:
+        return
     value = world * args.steps / (ms / 1e3)
     peaks, peak_src = measured_peaks()
-    kern_gbs = tim["bytes_hbm"] / (tim["total_ms"] / 1e3) / 1e9 if tim["total_ms"] > 0 else None
-    traffic = traffic_from_profiles(args.workload)
-    e2e = run_e2e(runner, args, torch)
+    hbm_step = sum(r["hbm"] for r in per_rank) / args.steps
+    nvl_step = sum(r["nvl"] for r in per_rank) / args.steps
+    loc_ms = sum(r["tim"]["local_ms"] for r in per_rank)
+    loc_b = sum(r["tim"]["local_bytes_hbm"] for r in per_rank)
+    x_ms = sum(r["tim"]["cross_ms"] for r in per_rank)
+    x_b = sum(r["tim"]["cross_bytes_nvlink"] for r in per_rank)
+    hbm_roof = None
+    if loc_ms > 0:
+        a = loc_b / (loc_ms / 1e3) / 1e9
+        hbm_roof = {"bound": "hbm", "kernel": "preduce_multi_kernel (fused SGD + P-Reduce, intra-GPU groups)",
+                    "achieved": round(a, 1), "peak": peaks["hbm_gbs"], "peak_source": peak_src, "unit": "GB/s",
+                    "frac": round(a / peaks["hbm_gbs"], 4),
+                    "traffic": traffic_from_profiles(args.workload, n_gpus),
+                    "launches": sum(r["tim"]["local_launches"] for r in per_rank),
+                    "kernel_ms_per_launch": round(loc_ms / max(1, sum(r["tim"]["local_launches"] for r in per_rank)), 4),
+                    "algorithmic_bytes_per_launch": int(loc_b / max(1, sum(r["tim"]["local_launches"] for r in per_rank)))}
+    nvl_roof = None
+    if x_ms > 0:
+        a = x_b / (x_ms / 1e3) / 1e9        # per GPU: its NVLink read bytes / its kernel time
+        nvl_roof = {"bound": "nvlink", "kernel": "xgpu_kernel (fused SGD + P-Reduce, cross-GPU part)",
+                    "achieved": round(a, 1), "peak": NVLINK_PEAK,
+                    "peak_source": "fallback (B200_PROFILING.md: measured peer copy per direction; 900 nominal)",
+                    "unit": "GB/s", "frac": round(a / NVLINK_PEAK, 4), "frac_of_nominal": round(a / NVLINK_NOMINAL, 4),
+                    "traffic": None,
+                    "launches": sum(r["tim"]["cross_launches"] for r in per_rank),
+                    "kernel_ms_per_launch": round(x_ms / max(1, sum(r["tim"]["cross_launches"] for r in per_rank)), 4),
+                    "algorithmic_nvlink_bytes_per_launch_per_gpu":
+                        int(x_b / max(1, sum(r["tim"]["cross_launches"] for r in per_rank)))}
+    # the dominant kernel is the one with the larger share of device time
+    roof = nvl_roof if (nvl_roof and x_ms >= loc_ms) else (hbm_roof or nvl_roof)
+    if roof is not None:
+        roof = dict(roof)
+        roof["other_kernel"] = hbm_roof if roof is nvl_roof else nvl_roof
+    clocks = [r["clocks"] for r in per_rank if r["clocks"]]
     out = {
         "metric": "worker-steps/s (P-Reduce GB/s vs NVLink/HBM roofline; worker-steps/sec at 1/2/4/8 B200)",
         "value": round(value, 1),
@@ -164,34 +248,83 @@ def run_ours(args, wl):
         "dtype": "f32",
         "data": "synthetic (counter-based xi generator; resident replicas + gradients)",
         "impl": "ours",
-        "preduce_gbs": round(bytes_step * args.steps / (ms / 1e3) / 1e9, 1),
+        "preduce_gbs": round((hbm_step + nvl_step) * args.steps / (ms / 1e3) / 1e9, 1),
         "config": {"workload": args.workload, "desc": wl["desc"], "world": world, "workers_per_gpu": wpg,
                    "n_params": n, "group_size": k, "schedule": wl["rule"] or "GB+GD (lockstep, ascending requests)",
-                   "lr": 0.1, "bytes_per_step": int(bytes_step),
-                   "l2": ("inputs larger than L2" if bytes_step > L2_BYTES else
+                   "lr": 0.1, "hbm_bytes_per_step": int(hbm_step), "nvlink_bytes_per_step": int(nvl_step),
+                   "cross_gpu_groups_per_step": sum(r["cross"] for r in per_rank) / args.steps,
+                   "parallelism": f"{n_gpus} ranks x {wpg} workers, disjoint groups",
+                   "l2": ("inputs larger than L2" if hbm_step / n_gpus > L2_BYTES else
                           "working set fits in L2 (no flush): L2-resident number")},
-        "roofline": {"bound": "hbm", "kernel": "preduce_multi_kernel (fused SGD + P-Reduce)",
-                     "achieved": round(kern_gbs, 1) if kern_gbs else None, "peak": peaks["hbm_gbs"],
-                     "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(kern_gbs / peaks["hbm_gbs"], 4) if kern_gbs else None,
-                     "traffic": traffic, "launches_per_step": launches / args.steps,
-                     "kernel_ms_per_launch": round(tim["total_ms"] / max(tim["launches"], 1), 4),
-                     "algorithmic_bytes_per_launch": int(tim["bytes_hbm"] / max(tim["launches"], 1))},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "roofline": roof,
+        "gpu_launches": sum(r["launches"] for r in per_rank),
+        "clocks": clocks[0] if len(clocks) == 1 else {
+            "sm_mhz": statistics.median(c["sm_mhz"] for c in clocks),
+            "sm_max_mhz": max(c["sm_max_mhz"] for c in clocks),
+            "reasons": sorted({x for c in clocks for x in c["reasons"]}), "per_rank": clocks} if clocks else None,
         "e2e": e2e,
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if n_gpus == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, n_gpus, budget_s=args.cpu_budget)
-    runner.close()
+    print(json.dumps(out), flush=True)
+
+
+def run_nccl_ar(args, wl):
+    """Baseline: global All-Reduce (Horovod/NCCL in the paper) of every
+    worker's SGD-updated replica: local SGD + pre-sum of the GPU's workers, ncclAllReduce(sum),
+    divide by the world size, write back to every local replica (torch ops + NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, local_rank, n_gpus = init_dist(args)
+    torch.cuda.set_device(local_rank)
+    if n_gpus > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        pg = dist.new_group(backend="gloo")
+    else:
+        pg = None
+    wpg, n = wl["wpg"], wl["n"]
+    world = wpg * n_gpus
+    X = torch.rand((wpg, n), device="cuda") * 2 - 1
+    G = torch.rand((wpg, n), device="cuda") * 2 - 1
+    lr = 0.1
+
+    def step():
+        X.sub_(G, alpha=lr)
+        s = X.sum(0) if wpg > 1 else X[0].clone()
+        if n_gpus > 1:
+            dist.all_reduce(s)
+        s.div_(world)
+        X.copy_(s.expand_as(X))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(pg)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(pg)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), pg)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        bus = 2 * (n_gpus - 1) / n_gpus * 4 * n if n_gpus > 1 else 0
+        print(json.dumps({
+            "metric": "worker-steps/s (P-Reduce GB/s vs NVLink/HBM roofline; worker-steps/sec at 1/2/4/8 B200)",
+            "value": round(world * args.steps / (ms / 1e3), 1), "unit": "worker-steps/s", "n_gpus": n_gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "dtype": "f32", "impl": "nccl-allreduce-baseline",
+            "busbw_gbs": round(bus * args.steps / (ms / 1e3) / 1e9, 1) if bus else None,
+            "config": {"workload": args.workload, "world": world, "workers_per_gpu": wpg, "n_params": n}}),
+            flush=True)
 
 
-def run_e2e(runner, args, torch):
+def run_e2e(runner, args, torch, pg):
     """Same metric through the public API with host buffers: per step, h2d of every local worker's
     gradient from pinned host memory, the lockstep step, and a blocking d2h read of the step's
-    result (the first 4 averaged parameters of every local worker)."""
+    result (the first 4 averaged parameters of every local worker). Max over ranks."""
     steps = max(1, min(args.steps, args.e2e_steps))
     n = runner.n
     host_g = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in runner.local]
@@ -200,6 +333,7 @@ def run_e2e(runner, args, torch):
     host_out = torch.empty((len(runner.local), 4), dtype=torch.float32, pin_memory=True)
     runner.synchronize()
     streams = {w: torch.cuda.ExternalStream(runner.streams[w]) for w in runner.local}
+    barrier(pg)
     t0 = time.perf_counter()
     for _ in range(steps):
         for i, w in enumerate(runner.local):
@@ -211,20 +345,21 @@ def run_e2e(runner, args, torch):
                 host_out[i].copy_(runner.x(w)[:4], non_blocking=True)
         for w in runner.local:
             streams[w].synchronize()
-    dt = time.perf_counter() - t0
-    return {"value": round(len(runner.local) * runner.ctx.cfg.n_gpus * steps / dt, 1) if dt > 0 else None,
+    dt = max_over_ranks(time.perf_counter() - t0, pg)
+    return {"value": round(runner.world * steps / dt, 1) if dt > 0 else None,
             "unit": "worker-steps/s", "steps": steps,
-            "h2d_bytes_per_step": 4 * n * len(runner.local),
-            "d2h_bytes_per_step": 16 * len(runner.local),
-            "timer": "host wall clock around the public-API steps (includes pinned h2d/d2h)"}
+            "h2d_bytes_per_step": 4 * n * runner.world,
+            "d2h_bytes_per_step": 16 * runner.world,
+            "timer": "host wall clock around the public-API steps (includes pinned h2d/d2h), max over ranks"}
 
 
-def traffic_from_profiles(workload):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+def traffic_from_profiles(workload, n_gpus):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed ncu --set full capture of this workload (profiles/traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(workload)
+            return json.load(f).get(f"{workload}@{n_gpus}")
     except (OSError, ValueError):
         return None
 
@@ -323,7 +458,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--impl", choices=["ours", "reference", "nccl"], default="ours",
+                    help="ours | reference (CPU oracle) | nccl (global all-reduce baseline)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -336,6 +472,8 @@ def main():
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl)
+    elif args.impl == "nccl":
+        run_nccl_ar(args, wl)
     else:
         run_ours(args, wl)
 

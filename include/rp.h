@@ -46,6 +46,8 @@ extern "C" {
 #define RP_MAX_WORLD 64 /* lock vector is one uint64_t, one bit per worker */
 #define RP_MAX_GROUP 16 /* largest group a P-Reduce accepts */
 #define RP_MAX_GPUS 8   /* GPUs of one NVSwitch node */
+#define RP_MAX_LOCAL 16 /* workers per GPU in a multi-GPU job */
+#define RP_IPC_HANDLE_BYTES 64
 
 /* ---- status codes ---------------------------------------------------------- */
 #define RP_OK 0
@@ -111,7 +113,14 @@ typedef struct rp_timing {
   double total_ms;            /* sum of per-launch durations                           */
   double min_ms, max_ms;
   int64_t bytes_hbm;          /* algorithmic HBM bytes of those launches               */
-  int64_t bytes_nvlink;       /* algorithmic NVLink bytes of those launches            */
+  int64_t bytes_nvlink;       /* algorithmic NVLink bytes read by this GPU             */
+  /* split by kernel: intra-GPU groups (HBM-bound) and cross-GPU parts (NVLink-bound) */
+  int64_t local_launches;
+  double local_ms;
+  int64_t local_bytes_hbm;
+  int64_t cross_launches;
+  double cross_ms;
+  int64_t cross_bytes_nvlink;
 } rp_timing;
 
 typedef struct rp_ctx rp_ctx;
@@ -142,6 +151,31 @@ int rp_bind_worker(rp_ctx* ctx, int32_t w, float* x_dev, const float* g_dev);
  * the averaged replica. Library-owned unless replaced by rp_set_worker_stream. */
 int rp_worker_stream(rp_ctx* ctx, int32_t w, void** stream_out);
 int rp_set_worker_stream(rp_ctx* ctx, int32_t w, void* stream);
+
+/* ---- multi-GPU: peer memory over NVLink / NVSwitch ----------------------------------
+ * A group whose members live on several GPUs runs as one exchange step over
+ * peer memory: every rank must map its peers' replicas and flag
+ * arrays. After binding all local workers, each rank calls rp_peer_export,
+ * the caller exchanges the records (e.g. torch.distributed.all_gather_object)
+ * and every rank calls rp_peer_import with the records of ALL ranks. */
+typedef struct rp_peer_info {
+  int32_t rank;            /* GPU index of the exporting rank                         */
+  int32_t n_local;         /* local workers exported (= workers_per_gpu)              */
+  int32_t first_worker;    /* rank * workers_per_gpu                                  */
+  int32_t pid;             /* exporting process id (diagnostics)                      */
+  uint8_t flags_handle[RP_IPC_HANDLE_BYTES];  /* cudaIpcMemHandle_t of the flag array  */
+  int64_t flags_offset;
+  uint8_t x_handle[RP_MAX_LOCAL][RP_IPC_HANDLE_BYTES]; /* allocation holding replica i */
+  int64_t x_offset[RP_MAX_LOCAL];                       /* byte offset of replica i      */
+} rp_peer_info;
+
+/* Fill *out with CUDA IPC handles for this rank's flag array and the replicas
+ * of its local workers (all must be bound). Errors: RP_ESTATE (unbound worker,
+ * single-GPU context), RP_ECUDA (the replica memory cannot be shared). */
+int rp_peer_export(rp_ctx* ctx, rp_peer_info* out);
+/* Map the peers' memory (infos[i] for every rank i, own record ignored).
+ * Errors: RP_EINVAL (missing / inconsistent records), RP_ECUDA. */
+int rp_peer_import(rp_ctx* ctx, const rp_peer_info* infos, int32_t n);
 
 /* ---- Step 3: group determination -------------------------------------------------- */
 
@@ -176,6 +210,13 @@ int rp_group_generate(rp_ctx* ctx, int32_t w, rp_group* out);
  * host-only contexts. Errors: RP_EPROTO (unknown group, not at the head of a
  * member's GB, or a member that never requested it). */
 int rp_gg_release(rp_ctx* ctx, int64_t seq);
+
+/* Lockstep convenience: rp_group_generate for workers[0..n-1] in that order
+ * (one GG critical section), out[i] = the group of workers[i]. Multi-GPU
+ * lockstep runs issue the same call on every rank to keep the replicated GG
+ * identical. Errors as rp_group_generate (requests before the failing one
+ * stay granted). */
+int rp_group_generate_many(rp_ctx* ctx, const int32_t* workers, int32_t n, rp_group* out);
 
 /* Worker w will not request again after its current group (reading R19: a
  * finished worker must never be put into a Global Division). */

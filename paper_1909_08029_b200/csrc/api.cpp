@@ -116,9 +116,17 @@ struct rp_ctx {
   struct Timed {
     cudaEvent_t start, stop;
     int64_t bytes_hbm, bytes_nvlink;
+    bool cross;
   };
   std::vector<Timed> timed;           // recorded, not yet read
   std::vector<cudaEvent_t> event_pool;  // timing events for reuse
+  // multi-GPU
+  unsigned long long* flags = nullptr;     // this GPU's flag array (IPC-exported)
+  unsigned long long* counters = nullptr;  // phase counters (local only)
+  bool peers_ready = false;
+  float* peer_x[RP_MAX_WORLD] = {};                 // replicas of remote workers, mapped
+  unsigned long long* peer_flags[RP_MAX_GPUS] = {};  // flag arrays of the other GPUs, mapped
+  std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
 };
 
 namespace {
@@ -184,18 +192,20 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // local (caller holds mu). The kernel runs on the stream of the lowest local
 // member after every member's arrival event; every member's stream is then
 // ordered after the kernel and records its own completion event.
-int launch_groups(rp_ctx* c, const std::vector<int64_t>& seqs) {
-  if (seqs.empty()) return RP_OK;
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream);
+
+int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
+  if (all_seqs.empty()) return RP_OK;
+  std::vector<int64_t> seqs, cross;
+  for (int64_t q : all_seqs) (c->active.at(q).local_mask == c->active.at(q).members_mask ? seqs : cross).push_back(q);
   uint64_t all = 0;
-  for (int64_t q : seqs) {
+  for (int64_t q : all_seqs) {
     ActiveGroup& a = c->active.at(q);
-    if (a.local_mask != a.members_mask)
-      return fail(RP_EINVAL, "group " + members_str(a.g) + " spans GPUs; cross-GPU groups need the peer engine");
     c->stats.lock_assertions++;
-    if ((c->inflight | all) & a.members_mask)  // a member is still inside another group
+    if ((c->inflight | all) & a.local_mask)  // a member is still inside another group
       return fail(RP_ECONFLICT, "atomicity violation: members " + members_str(a.g, c->inflight | all) +
                                     " hold an unfinished group");
-    all |= a.members_mask;
+    all |= a.local_mask;
   }
   int launcher = __builtin_ctzll(all);
   WorkerSlot& L = c->w[launcher];
@@ -238,10 +248,14 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& seqs) {
     if (rc != RP_OK) return fail(rc, err);
     if (timing) {
       CUDA_TRY(cudaEventRecord(e1, L.stream));
-      c->timed.push_back({e0, e1, bytes, 0});
+      c->timed.push_back({e0, e1, bytes, 0, false});
     }
     c->stats.kernel_launches++;
     c->stats.bytes_hbm += bytes;
+  }
+  if (!cross.empty()) {
+    const int rc = launch_cross(c, cross, L.stream);
+    if (rc != RP_OK) return rc;
   }
   CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
   for (int m = 0; m < RP_MAX_WORLD; ++m) {
@@ -250,9 +264,108 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& seqs) {
     if (m != launcher) CUDA_TRY(cudaStreamWaitEvent(s.stream, L.ev_group, 0));
     CUDA_TRY(cudaEventRecord(s.ev_done, s.stream));
   }
-  for (int64_t q : seqs) c->active.at(q).launched = true;
+  for (int64_t q : all_seqs) c->active.at(q).launched = true;
   c->inflight |= all;
   c->cv.notify_all();
+  return RP_OK;
+}
+
+// This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch
+// (caller holds mu; members' arrival events already joined into `stream`).
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream) {
+  if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
+  if (static_cast<int>(seqs.size()) > rp::kMaxXParts)
+    return fail(RP_EINVAL, "more than 8 cross-GPU groups on one GPU in one step");
+  const int wpg = c->cfg.workers_per_gpu;
+  rp::XTask T{};
+  T.nparts = static_cast<int32_t>(seqs.size());
+  T.my_gpu = c->cfg.rank;
+  T.n = c->cfg.n_params;
+  T.my_flags = c->flags;
+  T.my_counters = c->counters;
+  for (size_t pi = 0; pi < seqs.size(); ++pi) {
+    ActiveGroup& a = c->active.at(seqs[pi]);
+    rp::XPart& p = T.part[pi];
+    p.k_total = a.g.size;
+    p.slot = a.g.members[0];
+    p.tag = a.g.seq >= 0 ? static_cast<uint64_t>(a.g.seq) + 1 : static_cast<uint64_t>(a.g.seq);
+    int last_gpu = -1;
+    for (int i = 0; i < a.g.size; ++i) {
+      const int m = a.g.members[i];
+      const int gpu = m / wpg;
+      if (gpu != last_gpu) {  // first (lowest) member on this GPU: its replica holds the GPU's partial
+        if (p.kp >= rp::kMaxXGpus) return fail(RP_EINVAL, "group spans more than 8 GPUs");
+        p.gpu[p.kp] = gpu;
+        if (gpu == c->cfg.rank) {
+          p.me = p.kp;
+          p.src[p.kp] = c->w[m].x;
+          p.pflags[p.kp] = c->flags;
+        } else {
+          p.src[p.kp] = c->peer_x[m];
+          p.pflags[p.kp] = c->peer_flags[gpu];
+        }
+        p.kp++;
+        last_gpu = gpu;
+      }
+      if (gpu == c->cfg.rank) {
+        if (p.m >= rp::kMaxXLocal) return fail(RP_EINVAL, "more than 8 local members in a cross-GPU group");
+        p.x[p.m] = c->w[m].x;
+        p.g[p.m] = a.grad[i];
+        p.lr[p.m] = a.lr[i];
+        p.m++;
+      }
+    }
+    c->stats.groups_launched++;
+    c->stats.cross_gpu_groups++;
+  }
+  const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing) {
+    e0 = timing_event(c);
+    e1 = timing_event(c);
+    if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
+    CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  std::string err;
+  const int rc = rp::launch_xgpu(T, stream, &err);
+  if (rc != RP_OK) return fail(rc, err);
+  // algorithmic bytes of this GPU's parts (geometry filled by the launcher)
+  int64_t nvl = 0, hbm = 0;
+  for (int pi = 0; pi < T.nparts; ++pi) {
+    const rp::XPart& p = T.part[pi];
+    const int64_t lo = std::min<int64_t>(p.me * p.S4, p.n4), hi = std::min<int64_t>((p.me + 1) * p.S4, p.n4);
+    int64_t mine = 4 * (hi - lo);
+    if (p.me == p.kp - 1) mine += p.rem;
+    const int64_t others = T.n - mine;
+    nvl += 4 * ((p.kp - 1) * mine + others);            // B: peers' partials; C: owners' means
+    int64_t rd = 0;
+    for (int m = 0; m < p.m; ++m) rd += p.g[m] ? 8 : 4;
+    hbm += rd * T.n + 4 * others * ((p.m > 1 || p.g[0]) ? 1 : 0) + 4 * p.m * T.n;  // A+B reads, A partial, B+C stores
+  }
+  if (timing) {
+    CUDA_TRY(cudaEventRecord(e1, stream));
+    c->timed.push_back({e0, e1, hbm, nvl, true});
+  }
+  c->stats.kernel_launches++;
+  c->stats.bytes_hbm += hbm;
+  c->stats.bytes_nvlink += nvl;
+  return RP_OK;
+}
+
+using CuMemGetAddressRange = int (*)(uintptr_t*, size_t*, uintptr_t);
+
+// Allocation base of a device pointer (driver entry point; no link-time libcuda).
+int allocation_base(const void* p, uintptr_t* base) {
+  static CuMemGetAddressRange fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+      return fail(RP_ECUDA, "cuMemGetAddressRange entry point unavailable");
+    fn = reinterpret_cast<CuMemGetAddressRange>(f);
+  }
+  size_t size = 0;
+  if (fn(base, &size, reinterpret_cast<uintptr_t>(p)) != 0) return fail(RP_ECUDA, "cuMemGetAddressRange failed");
   return RP_OK;
 }
 
@@ -328,8 +441,97 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       }
       s.own_stream = true;
     }
+    if (k.n_gpus > 1) {
+      if (wpg > RP_MAX_LOCAL) {
+        rp_finalize(c);
+        return fail(RP_EINVAL, "rp_init: at most 16 workers per GPU in a multi-GPU job");
+      }
+      if ((e = cudaMalloc(&c->flags, rp::kFlagWords * 8)) != cudaSuccess ||
+          (e = cudaMemset(c->flags, 0, rp::kFlagWords * 8)) != cudaSuccess ||
+          (e = cudaMalloc(&c->counters, rp::kCounterWords * 8)) != cudaSuccess ||
+          (e = cudaMemset(c->counters, 0, rp::kCounterWords * 8)) != cudaSuccess) {
+        rp_finalize(c);
+        return cuda_fail(e, "rp_init: flag buffers");
+      }
+    }
   }
   *out = c;
+  return RP_OK;
+}
+
+int rp_peer_export(rp_ctx* c, rp_peer_info* out) {
+  if (!c || !out) return fail(RP_EINVAL, "null argument");
+  if (!c->has_gpu || c->cfg.n_gpus < 2 || !c->flags) return fail(RP_ESTATE, "rp_peer_export: not a multi-GPU context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->cfg.device);
+  std::memset(out, 0, sizeof(*out));
+  const int wpg = c->cfg.workers_per_gpu;
+  out->rank = c->cfg.rank;
+  out->n_local = wpg;
+  out->first_worker = c->cfg.rank * wpg;
+  out->pid = 0;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->flags));
+  std::memcpy(out->flags_handle, &h, sizeof(h));
+  out->flags_offset = 0;
+  for (int i = 0; i < wpg; ++i) {
+    const WorkerSlot& s = c->w[out->first_worker + i];
+    if (!s.bound) return fail(RP_ESTATE, "rp_peer_export: worker " + std::to_string(out->first_worker + i) + " not bound");
+    uintptr_t base = 0;
+    const int rc = allocation_base(s.x, &base);
+    if (rc != RP_OK) return rc;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(out->x_handle[i], &h, sizeof(h));
+    out->x_offset[i] = static_cast<int64_t>(reinterpret_cast<uintptr_t>(s.x) - base);
+  }
+  return RP_OK;
+}
+
+int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
+  if (!c || !infos) return fail(RP_EINVAL, "null argument");
+  if (!c->has_gpu || c->cfg.n_gpus < 2 || !c->flags) return fail(RP_ESTATE, "rp_peer_import: not a multi-GPU context");
+  if (n != c->cfg.n_gpus) return fail(RP_EINVAL, "rp_peer_import: need one record per GPU");
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->cfg.device);
+  const int wpg = c->cfg.workers_per_gpu;
+  bool seen[RP_MAX_GPUS] = {};
+  // distinct allocations are opened once (several replicas may share one)
+  std::vector<std::pair<std::string, void*>> opened;
+  auto open = [&](const uint8_t* hb, void** out) -> int {
+    const std::string key(reinterpret_cast<const char*>(hb), RP_IPC_HANDLE_BYTES);
+    for (auto& kv : opened)
+      if (kv.first == key) {
+        *out = kv.second;
+        return RP_OK;
+      }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb, sizeof(h));
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    opened.emplace_back(key, p);
+    c->ipc_mapped.push_back(p);
+    *out = p;
+    return RP_OK;
+  };
+  for (int i = 0; i < n; ++i) {
+    const rp_peer_info& r = infos[i];
+    if (r.rank < 0 || r.rank >= n || seen[r.rank] || r.n_local != wpg || r.first_worker != r.rank * wpg)
+      return fail(RP_EINVAL, "rp_peer_import: inconsistent record for rank " + std::to_string(r.rank));
+    seen[r.rank] = true;
+    if (r.rank == c->cfg.rank) continue;
+    void* fb = nullptr;
+    int rc = open(r.flags_handle, &fb);
+    if (rc != RP_OK) return rc;
+    c->peer_flags[r.rank] = reinterpret_cast<unsigned long long*>(static_cast<char*>(fb) + r.flags_offset);
+    for (int j = 0; j < wpg; ++j) {
+      void* xb = nullptr;
+      rc = open(r.x_handle[j], &xb);
+      if (rc != RP_OK) return rc;
+      c->peer_x[r.first_worker + j] = reinterpret_cast<float*>(static_cast<char*>(xb) + r.x_offset[j]);
+    }
+  }
+  c->peers_ready = true;
   return RP_OK;
 }
 
@@ -342,6 +544,9 @@ int rp_finalize(rp_ctx* c) {
       cudaEventDestroy(t.stop);
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+    if (c->flags) cudaFree(c->flags);
+    if (c->counters) cudaFree(c->counters);
     for (auto& s : c->w) {
       if (s.stream) cudaStreamSynchronize(s.stream);
       if (s.ev_arrive) cudaEventDestroy(s.ev_arrive);
@@ -443,6 +648,18 @@ int rp_group_generate(rp_ctx* c, int32_t w, rp_group* out) {
   return RP_OK;
 }
 
+int rp_group_generate_many(rp_ctx* c, const int32_t* workers, int32_t n, rp_group* out) {
+  if (!c || (n > 0 && (!workers || !out)) || n < 0) return fail(RP_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  for (int i = 0; i < n; ++i) {
+    const int rc = rp::gg_request(&c->gg, workers[i], &out[i]);
+    if (rc != RP_OK) return rc;
+    c->stats.gg_requests++;
+    trace_line(c, "{\"ev\":\"req\",\"w\":" + std::to_string(workers[i]) + "," + group_json(out[i]) + "}");
+  }
+  return RP_OK;
+}
+
 int rp_gg_release(rp_ctx* c, int64_t seq) {
   if (!c) return fail(RP_EINVAL, "null ctx");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -512,6 +729,9 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
   }
   ActiveGroup& a = it->second;
   if ((a.arrived >> w) & 1) return fail(RP_EPROTO, "rp_preduce: worker arrived twice");
+  if (a.local_mask != a.members_mask && !c->batching)
+    return fail(RP_ESTATE, "rp_preduce: a cross-GPU group must be issued inside rp_batch_begin/end "
+                           "(one launch per GPU and step keeps the GPUs' launch orders consistent)");
   int idx = 0;
   while (g->members[idx] != w) ++idx;
   a.grad[idx] = s.staged ? s.grad : nullptr;
@@ -620,6 +840,15 @@ int rp_timing_read(rp_ctx* c, rp_timing* out) {
     r.max_ms = std::max<double>(r.max_ms, ms);
     r.bytes_hbm += t.bytes_hbm;
     r.bytes_nvlink += t.bytes_nvlink;
+    if (t.cross) {
+      r.cross_launches++;
+      r.cross_ms += ms;
+      r.cross_bytes_nvlink += t.bytes_nvlink;
+    } else {
+      r.local_launches++;
+      r.local_ms += ms;
+      r.local_bytes_hbm += t.bytes_hbm;
+    }
     c->event_pool.push_back(t.start);
     c->event_pool.push_back(t.stop);
   }

@@ -68,6 +68,46 @@ struct MultiTask {
 
 // Fused SGD + P-Reduce of groups whose members all live on the current GPU.
 int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::string* err);
+// ---- cross-GPU parts (xgpu.cu) ----------------------------------------------------------
+constexpr int kMaxXParts = 8;    // cross-GPU groups one GPU takes part in, per launch
+constexpr int kMaxXLocal = 8;    // local members of one cross-GPU group
+constexpr int kMaxXGpus = 8;     // GPUs of one group
+constexpr int kFlagSlots = 64;   // slot = lowest member of the group
+constexpr int kFlagSrc = 8;      // source GPU
+constexpr int kFlagPhases = 4;
+constexpr int kPhaseA = 0, kPhaseB = 1, kPhaseC = 2;
+constexpr size_t kFlagWords = static_cast<size_t>(kFlagSlots) * kFlagSrc * kFlagPhases;
+constexpr size_t kCounterWords = static_cast<size_t>(kFlagSlots) * kFlagPhases;
+
+struct XPart {
+  int32_t m;          // local members (ascending worker id)
+  int32_t kp;         // GPUs in the group
+  int32_t me;         // this GPU's index among them (ascending GPU id)
+  int32_t k_total;    // |G|
+  int32_t slot;       // flag slot
+  int32_t rem;        // n mod 4 (filled by the launcher)
+  uint64_t tag;       // nonzero, unique per group
+  int64_t n4, S4, ta, tb;   // geometry (filled by the launcher)
+  float* x[kMaxXLocal];
+  const float* g[kMaxXLocal];
+  float lr[kMaxXLocal];
+  const float* src[kMaxXGpus];            // x_first of each group GPU (peer-mapped or local)
+  unsigned long long* pflags[kMaxXGpus];  // flag array of each group GPU (peer-mapped or local)
+  int32_t gpu[kMaxXGpus];                 // GPU ids, ascending
+};
+
+struct XTask {
+  int32_t nparts;
+  int32_t my_gpu;
+  int64_t n;
+  int64_t b_begin, c_begin, c_end;   // tile index ranges (filled by the launcher)
+  unsigned long long* my_flags;
+  unsigned long long* my_counters;
+  XPart part[kMaxXParts];
+};
+
+// This GPU's parts of the cross-GPU groups of one step, in ONE launch.
+int launch_xgpu(XTask& t, void* stream, std::string* err);
 int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                    void* stream, std::string* err);
 

@@ -86,10 +86,30 @@ class rp_stats(ctypes.Structure):
 
 class rp_timing(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("total_ms", ctypes.c_double), ("min_ms", ctypes.c_double),
-                ("max_ms", ctypes.c_double), ("bytes_hbm", ctypes.c_int64), ("bytes_nvlink", ctypes.c_int64)]
+                ("max_ms", ctypes.c_double), ("bytes_hbm", ctypes.c_int64), ("bytes_nvlink", ctypes.c_int64),
+                ("local_launches", ctypes.c_int64), ("local_ms", ctypes.c_double),
+                ("local_bytes_hbm", ctypes.c_int64), ("cross_launches", ctypes.c_int64),
+                ("cross_ms", ctypes.c_double), ("cross_bytes_nvlink", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+RP_MAX_LOCAL = 16
+RP_IPC_HANDLE_BYTES = 64
+
+
+class rp_peer_info(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("n_local", ctypes.c_int32),
+        ("first_worker", ctypes.c_int32),
+        ("pid", ctypes.c_int32),
+        ("flags_handle", ctypes.c_uint8 * RP_IPC_HANDLE_BYTES),
+        ("flags_offset", ctypes.c_int64),
+        ("x_handle", (ctypes.c_uint8 * RP_IPC_HANDLE_BYTES) * RP_MAX_LOCAL),
+        ("x_offset", ctypes.c_int64 * RP_MAX_LOCAL),
+    ]
 
 
 class RPError(RuntimeError):
@@ -107,11 +127,15 @@ _SIGNATURES = {
     "rp_bind_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, _P]),
     "rp_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(_P)]),
     "rp_set_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, _P]),
+    "rp_peer_export": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_peer_info)]),
+    "rp_peer_import": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_peer_info), ctypes.c_int32]),
     "rp_schedule_static": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "rp_schedule_static_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                                  ctypes.POINTER(rp_group)]),
     "rp_group_generate": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(rp_group)]),
+    "rp_group_generate_many": (ctypes.c_int, [_CTX, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                                              ctypes.POINTER(rp_group)]),
     "rp_gg_release": (ctypes.c_int, [_CTX, ctypes.c_int64]),
     "rp_retire": (ctypes.c_int, [_CTX, ctypes.c_int32]),
     "rp_step": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float]),
@@ -195,6 +219,21 @@ def rp_set_worker_stream(ctx, w, stream):
     _check(load_library().rp_set_worker_stream(ctx, w, _ptr(stream)), "rp_set_worker_stream")
 
 
+def rp_peer_export(ctx):
+    """Returns this rank's rp_peer_info as bytes (to exchange between ranks)."""
+    info = rp_peer_info()
+    _check(load_library().rp_peer_export(ctx, ctypes.byref(info)), "rp_peer_export")
+    return bytes(info)
+
+
+def rp_peer_import(ctx, records):
+    """records: list of rp_peer_export() byte strings, one per rank (any order)."""
+    arr = (rp_peer_info * len(records))()
+    for i, b in enumerate(records):
+        ctypes.memmove(ctypes.byref(arr[i]), b, ctypes.sizeof(rp_peer_info))
+    _check(load_library().rp_peer_import(ctx, arr, len(records)), "rp_peer_import")
+
+
 def rp_schedule_static(ctx, rule, step, world):
     arr = (ctypes.c_int32 * world)()
     ng = ctypes.c_int32()
@@ -213,6 +252,14 @@ def rp_group_generate(ctx, w):
     g = rp_group()
     _check(load_library().rp_group_generate(ctx, w, ctypes.byref(g)), "rp_group_generate")
     return g
+
+
+def rp_group_generate_many(ctx, workers):
+    n = len(workers)
+    arr = (ctypes.c_int32 * n)(*workers)
+    out = (rp_group * n)()
+    _check(load_library().rp_group_generate_many(ctx, arr, n, out), "rp_group_generate_many")
+    return list(out)
 
 
 def rp_gg_release(ctx, seq):
@@ -313,6 +360,21 @@ class Context:
     def bind_worker(self, w, x, g=None):
         rp_bind_worker(self.handle, w, x, g)
 
+    def peer_export(self):
+        return rp_peer_export(self.handle)
+
+    def peer_import(self, records):
+        rp_peer_import(self.handle, records)
+
+    def peer_setup(self, group=None):
+        """Exchange peer records over torch.distributed (metadata only; the data path is the
+        library's own NVLink peer loads) and map every peer's replicas and flags."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        records = [None] * dist.get_world_size(group)
+        dist.all_gather_object(records, mine, group=group)
+        self.peer_import(records)
+
     def worker_stream(self, w):
         return rp_worker_stream(self.handle, w)
 
@@ -327,6 +389,9 @@ class Context:
 
     def group_generate(self, w):
         return rp_group_generate(self.handle, w)
+
+    def group_generate_many(self, workers):
+        return rp_group_generate_many(self.handle, workers)
 
     def gg_release(self, seq):
         rp_gg_release(self.handle, seq)

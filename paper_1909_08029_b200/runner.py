@@ -32,7 +32,8 @@ def _ceil_to(v, m):
 
 class LockstepRunner:
     def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
-                 lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True):
+                 lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True,
+                 peer_group=None):
         if mode not in ("static", "gd"):
             raise ValueError("mode must be 'static' or 'gd'")
         if mode == "static" and rule not in RULES:
@@ -43,6 +44,7 @@ class LockstepRunner:
         torch.cuda.set_device(self.device)
         self.mode, self.rule, self.lr, self.grad_mode = mode, rule, lr, grad_mode
         self.world, self.n = world, n_params
+        self.n_gpus, self.peer_group = n_gpus, peer_group
         self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device,
                            group_size=group_size, c_thres=c_thres, nodes=nodes, seed_gd=seed_gd, flags=flags)
         self.local = self.ctx.local_workers()
@@ -54,6 +56,10 @@ class LockstepRunner:
         for i, w in enumerate(self.local):
             self.ctx.bind_worker(w, self.x(w), self.g(w))
             self.streams[w] = self.ctx.worker_stream(w)
+        if n_gpus > 1:
+            # map the peers' replicas + flag arrays (CUDA IPC records exchanged over
+            # torch.distributed; the data path is the library's NVLink kernel)
+            self.ctx.peer_setup(peer_group)
         self.t = 0
         if init:
             self.init_replicas()
@@ -90,8 +96,8 @@ class LockstepRunner:
         else:
             local = set(self.local)
             seen = set()
-            for w in range(self.world):           # same request order on every rank
-                g = self.ctx.group_generate(w)
+            # same request order (ascending) on every rank: the replicated GG stays identical
+            for w, g in zip(range(self.world), self.ctx.group_generate_many(list(range(self.world)))):
                 if w in local:
                     groups[w] = g
                 elif g.seq not in seen and not (set(g.member_list()) & local):
@@ -133,4 +139,9 @@ class LockstepRunner:
 
     def close(self):
         self.synchronize()
+        if self.n_gpus > 1:
+            # every rank's last kernel has seen its peers finish reading; the barrier keeps a
+            # rank from freeing replicas another rank still has mapped
+            import torch.distributed as dist
+            dist.barrier(group=self.peer_group)
         self.ctx.close()

@@ -1,0 +1,70 @@
+"""One rank of a multi-GPU parity run (launched by tests/test_gpu_multi.py through torchrun).
+
+Each rank drives its GPU's workers through the public API (cross-GPU groups run the
+NVLink peer kernel) and checks its local replicas against the CPU oracle bit for bit.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import sim  # noqa: E402
+from paper_1909_08029_b200.runner import LockstepRunner  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--wpg", type=int, required=True)
+    ap.add_argument("--n", type=int, required=True)
+    ap.add_argument("--k", type=int, required=True)
+    ap.add_argument("--mode", choices=["static", "gd"], required=True)
+    ap.add_argument("--rule", default=None)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--sample", type=int, default=0, help="compare only 3 slices of this length")
+    a = ap.parse_args()
+    dist.init_process_group("gloo")
+    rank, ngpu = dist.get_rank(), dist.get_world_size()
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    world = a.wpg * ngpu
+    nodes = ngpu if a.rule == "paper4" else 0
+    r = LockstepRunner(world, a.n, mode=a.mode, rule=a.rule, group_size=a.k, n_gpus=ngpu, rank=rank,
+                       device=local_rank, nodes=nodes)
+    log = r.run(a.steps)
+    r.synchronize()
+    slices = [(0, a.n)] if not a.sample else [(0, a.sample), (a.n // 2, a.n // 2 + a.sample),
+                                               (a.n - a.sample, a.n)]
+    ok = True
+    for lo, hi in slices:
+        X, olog = sim.run_lockstep(world, a.n, a.steps, mode=a.mode, rule=a.rule, k=a.k, nodes=nodes,
+                                   m=(world // nodes if nodes else None), workers_per_gpu=a.wpg, lo=lo, hi=hi)
+        for w in r.local:
+            got = r.x(w)[lo:hi].cpu().numpy()
+            if not np.array_equal(got.view(np.uint32), X[w].view(np.uint32)):
+                bad = np.flatnonzero(got.view(np.uint32) != X[w].view(np.uint32))
+                print(f"rank {rank} worker {w} slice [{lo},{hi}): {bad.size} elements differ, first {bad[:5]}, "
+                      f"max abs {np.max(np.abs(got - X[w]))}", flush=True)
+                ok = False
+    mine = [g for _, gs in log for g in gs]
+    olocal = [tuple(g) for _, gs in olog for g in sorted(gs) if set(g) & set(r.local)]
+    if sorted(mine) != sorted(olocal):
+        print(f"rank {rank}: group assignments differ from the oracle", flush=True)
+        ok = False
+    st = r.ctx.stats()
+    print(f"rank {rank}: {'OK' if ok else 'FAIL'} cross_gpu_groups={st['cross_gpu_groups']} "
+          f"launches={st['kernel_launches']}", flush=True)
+    flag = torch.tensor([0 if ok else 1])
+    dist.all_reduce(flag)
+    r.close()
+    dist.destroy_process_group()
+    sys.exit(int(flag.item() != 0))
+
+
+if __name__ == "__main__":
+    main()

@@ -41,13 +41,15 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layout_matches_c(tmp_path):
     prog = tmp_path / "sz.c"
     prog.write_text('#include "rp.h"\n#include <stdio.h>\n#include <stddef.h>\n'
-                    'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(rp_config), sizeof(rp_group),'
-                    ' sizeof(rp_stats), offsetof(rp_config, seed_gd), offsetof(rp_group, members));return 0;}\n')
+                    'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(rp_config), sizeof(rp_group),'
+                    ' sizeof(rp_stats), offsetof(rp_config, seed_gd), offsetof(rp_group, members),'
+                    ' sizeof(rp_timing), sizeof(rp_peer_info), offsetof(rp_peer_info, x_offset));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     assert got == [ctypes.sizeof(rp.rp_config), ctypes.sizeof(rp.rp_group), ctypes.sizeof(rp.rp_stats),
-                   rp.rp_config.seed_gd.offset, rp.rp_group.members.offset]
+                   rp.rp_config.seed_gd.offset, rp.rp_group.members.offset, ctypes.sizeof(rp.rp_timing),
+                   ctypes.sizeof(rp.rp_peer_info), rp.rp_peer_info.x_offset.offset]
 
 
 def test_init_validation_errors():

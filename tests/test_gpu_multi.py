@@ -1,0 +1,61 @@
+"""Multi-GPU parity (one process per GPU, cross-GPU groups over NVLink peer memory) vs the oracle.
+
+Runs only when the box exposes >= 2 GPUs (gpurun --gpus 2/4); each case launches torchrun.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N_R50 = 25_557_032
+
+
+def _ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(nproc, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "multi_gpu_worker.py")] + [str(a) for a in args]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert p.stdout.count("OK") == nproc, p.stdout
+
+
+CASES = [
+    # (gpus, wpg, n, k, mode, rule, steps, sample)
+    (2, 1, (1 << 20) + 3, 2, "static", "shift_k", 20, 0),     # one cross pair per step, ragged
+    (2, 2, 100_003, 3, "static", "shift_k", 12, 0),           # pre-reduction of co-resident members
+    (2, 4, 100_003, 3, "gd", None, 12, 0),                    # GB+GD: several cross parts per GPU
+    (2, 1, 5, 2, "static", "shift_k", 6, 0),                  # slices smaller than a tile
+    (2, 1, 1, 2, "static", "shift_k", 4, 0),                  # scalar-only
+    (2, 2, 65_536, 2, "static", "paper4", 8, 0),              # PAPER4 2 nodes x 2
+    (2, 1, N_R50, 2, "gd", None, 4, 4099),                    # ResNet-50 size, sampled
+    (4, 1, 200_003, 3, "gd", None, 10, 0),                    # cfg 3 shape at 4 GPUs
+    (4, 2, 200_003, 3, "static", "shift_k", 10, 0),           # cfg 4 shape at 4 GPUs
+    (4, 4, 60_001, 4, "static", "paper4", 8, 0),              # PAPER4 4 nodes x 4 (fig:schedule)
+]
+
+
+@pytest.mark.parametrize("gpus,wpg,n,k,mode,rule,steps,sample", CASES)
+def test_multi_gpu_parity(gpus, wpg, n, k, mode, rule, steps, sample):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    args = ["--wpg", wpg, "--n", n, "--k", k, "--mode", mode, "--steps", steps, "--sample", sample]
+    if rule:
+        args += ["--rule", rule]
+    _run(gpus, *args)
