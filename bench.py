@@ -165,8 +165,9 @@ def run_ours(args, wl):
     rank, local_rank, n_gpus = init_dist(args)
     torch.cuda.set_device(local_rank)
     pg = setup_dist(n_gpus, local_rank)
-    wpg, n, k = wl["wpg"], wl["n"], wl["k"]
+    wpg, n = wl["wpg"], wl["n"]
     world = wpg * n_gpus
+    k = min(wl["k"], world)              # e.g. configs[2] at 2 GPUs: 2 workers, groups of 2
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
                             rank=rank, device=local_rank, grad_mode="resident", flags=rp.RP_FLAG_TIMING,
                             peer_group=pg)
@@ -380,7 +381,8 @@ def oracle_steps(wl, n_gpus, sample, steps):
     world = wl["wpg"] * n_gpus
     X = {w: gen.x0(w, wl["n"], 0, sample) for w in range(world)}
     G = {w: gen.grad(w, 1, wl["n"], 0, sample) for w in range(world)}
-    gg = GroupGenerator(world, wl["k"], c_thres=4, seed_gd=3) if wl["mode"] == "gd" else None
+    k = min(wl["k"], world)
+    gg = GroupGenerator(world, k, c_thres=4, seed_gd=3) if wl["mode"] == "gd" else None
     lr = np.float32(0.1)
     t0 = time.perf_counter()
     for t in range(1, steps + 1):
@@ -393,7 +395,7 @@ def oracle_steps(wl, n_gpus, sample, steps):
             for s in sorted(seen):
                 gg.done(s)
         else:
-            groups = S.groups_for(wl["rule"], t, n=world, k=wl["k"])
+            groups = S.groups_for(wl["rule"], t, n=world, k=k)
             covered = {w for g in groups for w in g}
             groups = groups + [(w,) for w in range(world) if w not in covered]
         for g in groups:

@@ -4,6 +4,7 @@ Each rank drives its GPU's workers through the public API (cross-GPU groups run 
 NVLink peer kernel) and checks its local replicas against the CPU oracle bit for bit.
 """
 import argparse
+import json
 import os
 import sys
 
@@ -19,15 +20,8 @@ from paper_1909_08029_b200.runner import LockstepRunner  # noqa: E402
 
 
 def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--wpg", type=int, required=True)
-    ap.add_argument("--n", type=int, required=True)
-    ap.add_argument("--k", type=int, required=True)
-    ap.add_argument("--mode", choices=["static", "gd"], required=True)
-    ap.add_argument("--rule", default=None)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--sample", type=int, default=0, help="compare only 3 slices of this length")
-    a = ap.parse_args()
+    # one JSON positional argument (torchrun would try to parse --options after the script)
+    a = argparse.Namespace(**{"rule": None, "steps": 10, "sample": 0, **json.loads(sys.argv[1])})
     dist.init_process_group("gloo")
     rank, ngpu = dist.get_rank(), dist.get_world_size()
     local_rank = int(os.environ.get("LOCAL_RANK", rank))

@@ -2,6 +2,7 @@
 
 Runs only when the box exposes >= 2 GPUs (gpurun --gpus 2/4); each case launches torchrun.
 """
+import json
 import os
 import socket
 import subprocess
@@ -27,10 +28,10 @@ def _free_port():
     return p
 
 
-def _run(nproc, *args, timeout=600):
+def _run(nproc, spec, timeout=600):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tests", "multi_gpu_worker.py")] + [str(a) for a in args]
+           os.path.join(ROOT, "tests", "multi_gpu_worker.py"), json.dumps(spec)]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert p.stdout.count("OK") == nproc, p.stdout
@@ -55,7 +56,4 @@ CASES = [
 def test_multi_gpu_parity(gpus, wpg, n, k, mode, rule, steps, sample):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
-    args = ["--wpg", wpg, "--n", n, "--k", k, "--mode", mode, "--steps", steps, "--sample", sample]
-    if rule:
-        args += ["--rule", rule]
-    _run(gpus, *args)
+    _run(gpus, dict(wpg=wpg, n=n, k=k, mode=mode, rule=rule, steps=steps, sample=sample))
