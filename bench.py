@@ -230,10 +230,11 @@ def run_ours(args, wl):
                     "algorithmic_nvlink_bytes_per_launch_per_gpu":
                         int(x_b / max(1, sum(r["tim"]["cross_launches"] for r in per_rank)))}
     # the dominant kernel is the one with the larger share of device time
-    roof = nvl_roof if (nvl_roof and x_ms >= loc_ms) else (hbm_roof or nvl_roof)
+    main_is_nvl = bool(nvl_roof) and x_ms >= loc_ms
+    roof = nvl_roof if main_is_nvl else (hbm_roof or nvl_roof)
     if roof is not None:
         roof = dict(roof)
-        roof["other_kernel"] = hbm_roof if roof is nvl_roof else nvl_roof
+        roof["other_kernel"] = hbm_roof if main_is_nvl else nvl_roof
     clocks = [r["clocks"] for r in per_rank if r["clocks"]]
     out = {
         "metric": "worker-steps/s (P-Reduce GB/s vs NVLink/HBM roofline; worker-steps/sec at 1/2/4/8 B200)",

@@ -165,6 +165,9 @@ typedef struct rp_peer_info {
   int32_t pid;             /* exporting process id (diagnostics)                      */
   uint8_t flags_handle[RP_IPC_HANDLE_BYTES];  /* cudaIpcMemHandle_t of the flag array  */
   int64_t flags_offset;
+  uint8_t stage_handle[RP_IPC_HANDLE_BYTES];  /* staging buffer (partials pushed to it)  */
+  int64_t stage_offset;
+  int64_t stage_region_bytes;                 /* one region per local worker            */
   uint8_t x_handle[RP_MAX_LOCAL][RP_IPC_HANDLE_BYTES]; /* allocation holding replica i */
   int64_t x_offset[RP_MAX_LOCAL];                       /* byte offset of replica i      */
 } rp_peer_info;

@@ -122,10 +122,12 @@ struct rp_ctx {
   std::vector<cudaEvent_t> event_pool;  // timing events for reuse
   // multi-GPU
   unsigned long long* flags = nullptr;     // this GPU's flag array (IPC-exported)
-  unsigned long long* counters = nullptr;  // phase counters (local only)
+  float* stage = nullptr;                  // staging: one region per local worker (IPC-exported)
+  int64_t stage_region = 0;                // bytes per region
   bool peers_ready = false;
   float* peer_x[RP_MAX_WORLD] = {};                 // replicas of remote workers, mapped
   unsigned long long* peer_flags[RP_MAX_GPUS] = {};  // flag arrays of the other GPUs, mapped
+  float* peer_stage[RP_MAX_GPUS] = {};              // staging buffers of the other GPUs, mapped
   std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
 };
 
@@ -282,7 +284,6 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
   T.my_gpu = c->cfg.rank;
   T.n = c->cfg.n_params;
   T.my_flags = c->flags;
-  T.my_counters = c->counters;
   for (size_t pi = 0; pi < seqs.size(); ++pi) {
     ActiveGroup& a = c->active.at(seqs[pi]);
     rp::XPart& p = T.part[pi];
@@ -293,15 +294,19 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
     for (int i = 0; i < a.g.size; ++i) {
       const int m = a.g.members[i];
       const int gpu = m / wpg;
-      if (gpu != last_gpu) {  // first (lowest) member on this GPU: its replica holds the GPU's partial
+      if (gpu != last_gpu) {  // first (lowest) member on this GPU: receives the means, owns the region
         if (p.kp >= rp::kMaxXGpus) return fail(RP_EINVAL, "group spans more than 8 GPUs");
+        const int region = m - gpu * wpg;
         p.gpu[p.kp] = gpu;
         if (gpu == c->cfg.rank) {
           p.me = p.kp;
-          p.src[p.kp] = c->w[m].x;
+          p.xfirst[p.kp] = c->w[m].x;
+          p.stage[p.kp] = reinterpret_cast<float*>(reinterpret_cast<char*>(c->stage) + region * c->stage_region);
           p.pflags[p.kp] = c->flags;
         } else {
-          p.src[p.kp] = c->peer_x[m];
+          p.xfirst[p.kp] = c->peer_x[m];
+          p.stage[p.kp] =
+              reinterpret_cast<float*>(reinterpret_cast<char*>(c->peer_stage[gpu]) + region * c->stage_region);
           p.pflags[p.kp] = c->peer_flags[gpu];
         }
         p.kp++;
@@ -315,6 +320,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
         p.m++;
       }
     }
+    rp::xgpu_geometry(p, T.n);
     c->stats.groups_launched++;
     c->stats.cross_gpu_groups++;
   }
@@ -329,7 +335,8 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
   std::string err;
   const int rc = rp::launch_xgpu(T, stream, &err);
   if (rc != RP_OK) return fail(rc, err);
-  // algorithmic bytes of this GPU's parts (geometry filled by the launcher)
+  // algorithmic bytes of this GPU's parts: NVLink bytes this GPU stores into peers
+  // (A: its partials of the other slices; B: its slice's means to every peer)
   int64_t nvl = 0, hbm = 0;
   for (int pi = 0; pi < T.nparts; ++pi) {
     const rp::XPart& p = T.part[pi];
@@ -337,10 +344,11 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
     int64_t mine = 4 * (hi - lo);
     if (p.me == p.kp - 1) mine += p.rem;
     const int64_t others = T.n - mine;
-    nvl += 4 * ((p.kp - 1) * mine + others);            // B: peers' partials; C: owners' means
+    nvl += 4 * (others + (p.kp - 1) * mine);
     int64_t rd = 0;
     for (int m = 0; m < p.m; ++m) rd += p.g[m] ? 8 : 4;
-    hbm += rd * T.n + 4 * others * ((p.m > 1 || p.g[0]) ? 1 : 0) + 4 * p.m * T.n;  // A+B reads, A partial, B+C stores
+    // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
+    hbm += rd * T.n + 4 * (p.kp - 1) * mine + 4 * p.m * mine + 8 * (p.m - 1) * others;
   }
   if (timing) {
     CUDA_TRY(cudaEventRecord(e1, stream));
@@ -446,10 +454,10 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
         rp_finalize(c);
         return fail(RP_EINVAL, "rp_init: at most 16 workers per GPU in a multi-GPU job");
       }
+      c->stage_region = (rp::xgpu_stage_region_bytes(k.n_params) + 255) / 256 * 256;
       if ((e = cudaMalloc(&c->flags, rp::kFlagWords * 8)) != cudaSuccess ||
           (e = cudaMemset(c->flags, 0, rp::kFlagWords * 8)) != cudaSuccess ||
-          (e = cudaMalloc(&c->counters, rp::kCounterWords * 8)) != cudaSuccess ||
-          (e = cudaMemset(c->counters, 0, rp::kCounterWords * 8)) != cudaSuccess) {
+          (e = cudaMalloc(&c->stage, c->stage_region * wpg)) != cudaSuccess) {
         rp_finalize(c);
         return cuda_fail(e, "rp_init: flag buffers");
       }
@@ -474,6 +482,10 @@ int rp_peer_export(rp_ctx* c, rp_peer_info* out) {
   CUDA_TRY(cudaIpcGetMemHandle(&h, c->flags));
   std::memcpy(out->flags_handle, &h, sizeof(h));
   out->flags_offset = 0;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->stage));
+  std::memcpy(out->stage_handle, &h, sizeof(h));
+  out->stage_offset = 0;
+  out->stage_region_bytes = c->stage_region;
   for (int i = 0; i < wpg; ++i) {
     const WorkerSlot& s = c->w[out->first_worker + i];
     if (!s.bound) return fail(RP_ESTATE, "rp_peer_export: worker " + std::to_string(out->first_worker + i) + " not bound");
@@ -516,7 +528,8 @@ int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
   };
   for (int i = 0; i < n; ++i) {
     const rp_peer_info& r = infos[i];
-    if (r.rank < 0 || r.rank >= n || seen[r.rank] || r.n_local != wpg || r.first_worker != r.rank * wpg)
+    if (r.rank < 0 || r.rank >= n || seen[r.rank] || r.n_local != wpg || r.first_worker != r.rank * wpg ||
+        r.stage_region_bytes != c->stage_region)
       return fail(RP_EINVAL, "rp_peer_import: inconsistent record for rank " + std::to_string(r.rank));
     seen[r.rank] = true;
     if (r.rank == c->cfg.rank) continue;
@@ -524,6 +537,10 @@ int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
     int rc = open(r.flags_handle, &fb);
     if (rc != RP_OK) return rc;
     c->peer_flags[r.rank] = reinterpret_cast<unsigned long long*>(static_cast<char*>(fb) + r.flags_offset);
+    void* sb = nullptr;
+    rc = open(r.stage_handle, &sb);
+    if (rc != RP_OK) return rc;
+    c->peer_stage[r.rank] = reinterpret_cast<float*>(static_cast<char*>(sb) + r.stage_offset);
     for (int j = 0; j < wpg; ++j) {
       void* xb = nullptr;
       rc = open(r.x_handle[j], &xb);
@@ -546,7 +563,7 @@ int rp_finalize(rp_ctx* c) {
     for (auto e : c->event_pool) cudaEventDestroy(e);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (c->flags) cudaFree(c->flags);
-    if (c->counters) cudaFree(c->counters);
+    if (c->stage) cudaFree(c->stage);
     for (auto& s : c->w) {
       if (s.stream) cudaStreamSynchronize(s.stream);
       if (s.ev_arrive) cudaEventDestroy(s.ev_arrive);

@@ -74,10 +74,11 @@ constexpr int kMaxXLocal = 8;    // local members of one cross-GPU group
 constexpr int kMaxXGpus = 8;     // GPUs of one group
 constexpr int kFlagSlots = 64;   // slot = lowest member of the group
 constexpr int kFlagSrc = 8;      // source GPU
-constexpr int kFlagPhases = 4;
-constexpr int kPhaseA = 0, kPhaseB = 1, kPhaseC = 2;
-constexpr size_t kFlagWords = static_cast<size_t>(kFlagSlots) * kFlagSrc * kFlagPhases;
-constexpr size_t kCounterWords = static_cast<size_t>(kFlagSlots) * kFlagPhases;
+constexpr int kMaxChunks = 1024; // chunks per owner slice
+constexpr int64_t kMinChunkF4 = 2048;  // 32 KiB per buffer and chunk
+constexpr int kFlagA = 0, kFlagB = 1, kFlagReady = 2;
+constexpr int64_t kFlagStride = 2 * kMaxChunks + 1;  // A[chunk], B[chunk], READY
+constexpr size_t kFlagWords = static_cast<size_t>(kFlagSlots) * kFlagSrc * kFlagStride;
 
 struct XPart {
   int32_t m;          // local members (ascending worker id)
@@ -85,14 +86,15 @@ struct XPart {
   int32_t me;         // this GPU's index among them (ascending GPU id)
   int32_t k_total;    // |G|
   int32_t slot;       // flag slot
-  int32_t rem;        // n mod 4 (filled by the launcher)
+  int32_t rem;        // n mod 4
   uint64_t tag;       // nonzero, unique per group
-  int64_t n4, S4, ta, tb;   // geometry (filled by the launcher)
+  int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry)
   float* x[kMaxXLocal];
   const float* g[kMaxXLocal];
   float lr[kMaxXLocal];
-  const float* src[kMaxXGpus];            // x_first of each group GPU (peer-mapped or local)
-  unsigned long long* pflags[kMaxXGpus];  // flag array of each group GPU (peer-mapped or local)
+  float* xfirst[kMaxXGpus];               // first local member replica of each group GPU (mapped)
+  float* stage[kMaxXGpus];                // staging region of each group GPU for this group (mapped)
+  unsigned long long* pflags[kMaxXGpus];  // flag array of each group GPU (mapped or local)
   int32_t gpu[kMaxXGpus];                 // GPU ids, ascending
 };
 
@@ -100,12 +102,15 @@ struct XTask {
   int32_t nparts;
   int32_t my_gpu;
   int64_t n;
-  int64_t b_begin, c_begin, c_end;   // tile index ranges (filled by the launcher)
+  int64_t b_begin, c_begin, total_items;   // work-item ranges (filled by the launcher)
   unsigned long long* my_flags;
-  unsigned long long* my_counters;
   XPart part[kMaxXParts];
 };
 
+// Slice and chunk geometry of a part (kp set) for n elements.
+void xgpu_geometry(XPart& p, int64_t n);
+// Bytes of one staging region (one cross-GPU group owned by one local worker).
+int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
 int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,

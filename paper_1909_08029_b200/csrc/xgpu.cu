@@ -1,38 +1,44 @@
 // Cross-GPU fused SGD + P-Reduce: this GPU's part of groups whose members span
 // several GPUs of one NVSwitch node (one process per GPU, peer memory mapped
-// through CUDA IPC).
+// through CUDA IPC). Push-based and pipelined chunk by chunk.
 //
 // alg1 step 4 for a group G on GPUs d_0 < ... < d_{kp-1} is one
 // exchange step: a reduce-scatter + all-gather fused with the SGD of step 2
 // and with the pre-reduction of co-resident members. The element range
-// is cut into kp owner slices (tile-aligned float4 ranges); GPU d_i owns slice i.
+// is cut into kp owner slices (tile-aligned float4 ranges; GPU d_i owns slice
+// i) and every slice into nch chunks. Work items, in this order on every GPU:
 //
-//  A (HBM only)   for every slice o != mine: p_me = left fold over my local
-//                 members of y_m = fl(x_m - fl(lr_m g_m)) (ascending worker id),
-//                 stored in place into my first local member's replica
-//                 ("x_first"; the replicas are scratch while the group is in
-//                 flight). Then signal A-done to every peer.
-//  B (NVLink in)  for my slice: p_me in registers; for every other GPU d, wait
-//                 for its A-done and load its partial from its x_first over
-//                 NVLink; s = left fold of the partials in ascending GPU id;
-//                 xbar = fl(s / |G|) (reading R1); store xbar into all my local
-//                 members. Signal B-done.
-//  C (NVLink in)  for every slice o != mine: wait for owner o's B-done, load
-//                 xbar from o's x_first, store into all my local members.
-//                 Signal C-done once all my B and C tiles (every peer read) are
-//                 finished; the kernel ends only after every peer's C-done
-//                 (nobody may touch a replica a peer still reads).
-// NVLink bytes read per GPU: 2 (kp-1)/kp * 4N, the ring all-reduce bus bound.
+//  A (o, c)  o != me: p = left fold over my local members of
+//            y_m = fl(x_m - fl(lr_m g_m)) (ascending worker id) for chunk c of
+//            slice o, STORED OVER NVLINK into owner o's staging buffer (row me),
+//            then flag A[me][c] on owner o.
+//  B (c)     my slice: wait for A[d][c] from every peer d; own partial in
+//            registers, peers' partials from my staging (local HBM); s = left
+//            fold of the partials in ascending GPU id; xbar = fl(s / |G|)
+//            (reading R1); store xbar into my local members and OVER NVLINK into
+//            every peer's first local member ("x_first"), then flag B[me][c] on
+//            every peer.
+//  C (o, c)  o != me: wait for B[o][c]; xbar is already in my x_first; copy it
+//            to my other local members (nothing to do for a lone member).
 //
-// Synchronization: 64-bit tags in a per-GPU flag array (IPC-shared), written
-// by peers with st.release.sys and polled with ld.acquire.sys. Each CTA adds
-// its finished tiles of a phase to a local counter once (after a gpu-scope
-// fence); the CTA completing the phase issues a system fence and writes the
-// tag into every peer's flag array. The grid is at most the resident CTA count
-// so a CTA spinning on a flag never starves another CTA of this kernel.
+// No GPU ever reads peer memory: every NVLink byte is a store (bidirectional
+// peer stores measured ~700 GB/s/direction vs ~660 for loads on B200,
+// profiles/r01_nvlink_probe_2gpu.txt). NVLink bytes written per GPU:
+// 2 (kp-1)/kp * 4N, the ring all-reduce bus bound; the transfers of chunk c
+// overlap the compute of later chunks.
+//
+// Synchronization: 64-bit tags (unique per group) in per-GPU flag arrays
+// (IPC-shared), written with st.release.sys after a system fence and polled
+// with ld.acquire.sys. At kernel start each GPU posts READY to its peers; a GPU
+// pushes partials into an owner's staging only after the owner's READY (the
+// owner has finished its previous group, so the staging is free). The kernel
+// ends when all of this GPU's inbound A and B flags have been seen, i.e. when
+// no peer will write its memory for this group any more. The grid is at most
+// the resident CTA count, so a CTA spinning on a flag never starves another.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "rp_internal.h"
@@ -81,26 +87,16 @@ __device__ __forceinline__ float4 div4(float4 a, float k) {
   return make_float4(__fdiv_rn(a.x, k), __fdiv_rn(a.y, k), __fdiv_rn(a.z, k), __fdiv_rn(a.w, k));
 }
 
-__device__ __forceinline__ unsigned long long* flag_at(unsigned long long* base, int slot, int src, int phase) {
-  return base + (static_cast<int64_t>(slot) * kFlagSrc + src) * kFlagPhases + phase;
+// flag word of (slot, src GPU, kind, chunk) in a GPU's flag array
+__device__ __forceinline__ unsigned long long* flag_at(unsigned long long* base, int slot, int src, int kind,
+                                                       int64_t c) {
+  return base + (static_cast<int64_t>(slot) * kFlagSrc + src) * kFlagStride +
+         (kind == kFlagA ? c : (kind == kFlagB ? kMaxChunks + c : 2 * kMaxChunks));
 }
 
-// Geometry of part p: slice o is float4 range [o*S4, min((o+1)*S4, n4)); tiles of
-// kXThreads*U float4. The last slice also carries the n mod 4 scalar tail, which
-// gets an extra tile when the last regular tile is full (or the slice is empty).
-template <int U>
-struct Geo {
-  int64_t n4, S4;
-  int rem, kp;
-  __device__ __forceinline__ int64_t lo(int o) const { return min(static_cast<int64_t>(o) * S4, n4); }
-  __device__ __forceinline__ int64_t hi(int o) const { return min(static_cast<int64_t>(o + 1) * S4, n4); }
-  __device__ __forceinline__ int64_t tiles(int o) const {
-    const int64_t len = hi(o) - lo(o);
-    int64_t t = (len + kXThreads * U - 1) / (kXThreads * U);
-    if (o == kp - 1 && rem > 0 && len % (kXThreads * U) == 0) ++t;
-    return t;
-  }
-};
+__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long tag) {
+  while (ld_acquire_sys(f) != tag) __nanosleep(32);
+}
 
 // Local partial of my p.m (<= M) members at float4 index i (left fold, ascending worker id).
 template <int M>
@@ -128,238 +124,207 @@ __device__ __forceinline__ float local_partial1(const XPart& p, int64_t j) {
   return s;
 }
 
-__device__ __forceinline__ bool needs_partial_store(const XPart& p) {
-  return p.m > 1 || p.g[0] != nullptr;  // a lone member without a staged step: partial == x
+// Chunk c of slice o: float4 range [lo, hi); the last chunk of the last slice also
+// carries the n mod 4 scalar tail.
+struct ChunkRange {
+  int64_t lo, hi;
+  bool tail;
+};
+__device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) {
+  return min(static_cast<int64_t>(o) * p.S4, p.n4);
+}
+__device__ __forceinline__ ChunkRange chunk_range(const XPart& p, int o, int64_t c) {
+  const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
+  ChunkRange r;
+  r.lo = min(slo + c * p.CH, shi);
+  r.hi = min(slo + (c + 1) * p.CH, shi);
+  r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
+  return r;
 }
 
-template <int M>
-__device__ __forceinline__ void store_members4(const XPart& p, int64_t i, float4 v) {
-#pragma unroll
-  for (int m = 0; m < M; ++m)
-    if (m < p.m) stv(p.x[m] + 4 * i, v);
-}
-template <int M>
-__device__ __forceinline__ void store_members1(const XPart& p, int64_t j, float v) {
-#pragma unroll
-  for (int m = 0; m < M; ++m)
-    if (m < p.m) p.x[m][j] = v;
+// float offset of (row d, float4 index i relative to the slice start) in a staging
+// region: row d holds the partials GPU d sends for the owner's slice; S4 + 1 float4
+// per row so the tail scalars fit after the slice's float4 range.
+__device__ __forceinline__ int64_t stage_off(const XPart& p, int d, int64_t i_rel) {
+  return (static_cast<int64_t>(d) * (p.S4 + 1) + i_rel) * 4;
 }
 
-// ---- phase bodies over one tile ----------------------------------------------------------
 template <int M, int U>
-__device__ void tile_A(const XPart& p, const Geo<U>& geo, int o, int64_t t) {
-  const int64_t lo = geo.lo(o), hi = geo.hi(o);
-  const int64_t i0 = lo + t * kXThreads * U;
-  const bool store = needs_partial_store(p);
+__device__ void item_A(const XPart& p, int o, int64_t c) {
+  const ChunkRange r = chunk_range(p, o, c);
+  const int64_t slo = slice_lo(p, o);
+  float* dst = p.stage[o];  // owner o's staging region (peer memory)
+  for (int64_t t0 = r.lo; t0 < r.hi; t0 += kXThreads * U) {
+    float4 s[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = i0 + u * kXThreads + threadIdx.x;
-    if (i < hi) {
-      const float4 s = local_partial4<M>(p, i);
-      if (store) stv(p.x[0] + 4 * i, s);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) s[u] = local_partial4<M>(p, i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) stv(dst + stage_off(p, p.me, i - slo), s[u]);  // NVLink store
     }
   }
-  if (o == geo.kp - 1 && t == geo.tiles(o) - 1 && threadIdx.x < geo.rem) {
-    const int64_t j = 4 * geo.n4 + threadIdx.x;
-    const float s = local_partial1<M>(p, j);
-    if (store) p.x[0][j] = s;
+  if (r.tail && threadIdx.x < p.rem) {
+    const int64_t j = 4 * p.n4 + threadIdx.x;
+    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M>(p, j);
   }
 }
 
 template <int M, int U>
-__device__ void tile_B(const XPart& p, const Geo<U>& geo, int64_t t) {
+__device__ void item_B(const XPart& p, int64_t c) {
   const int o = p.me;
-  const int64_t lo = geo.lo(o), hi = geo.hi(o);
-  const int64_t i0 = lo + t * kXThreads * U;
+  const ChunkRange r = chunk_range(p, o, c);
+  const int64_t slo = slice_lo(p, o);
+  const float* stage = p.stage[o];  // my staging region (local)
   const float kf = static_cast<float>(p.k_total);
+  for (int64_t t0 = r.lo; t0 < r.hi; t0 += kXThreads * U) {
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = i0 + u * kXThreads + threadIdx.x;
-    if (i < hi) {
-      const float4 mine = local_partial4<M>(p, i);
-      float4 part[kMaxXGpus];
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) {
+        const float4 mine = local_partial4<M>(p, i);
+        float4 part[kMaxXGpus];
 #pragma unroll
-      for (int d = 0; d < kMaxXGpus; ++d)
-        if (d < p.kp && d != p.me) part[d] = ldv(p.src[d] + 4 * i);  // NVLink
-      float4 s = p.me == 0 ? mine : part[0];
+        for (int d = 0; d < kMaxXGpus; ++d)
+          if (d < p.kp && d != o) part[d] = ldv(stage + stage_off(p, d, i - slo));
+        float4 s = o == 0 ? mine : part[0];
 #pragma unroll
-      for (int d = 1; d < kMaxXGpus; ++d)
-        if (d < p.kp) s = add4(s, d == p.me ? mine : part[d]);
-      store_members4<M>(p, i, div4(s, kf));
+        for (int d = 1; d < kMaxXGpus; ++d)
+          if (d < p.kp) s = add4(s, d == o ? mine : part[d]);
+        const float4 xbar = div4(s, kf);
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          if (m < p.m) stv(p.x[m] + 4 * i, xbar);
+#pragma unroll
+        for (int d = 0; d < kMaxXGpus; ++d)
+          if (d < p.kp && d != o) stv(p.xfirst[d] + 4 * i, xbar);  // NVLink store
+      }
     }
   }
-  if (o == geo.kp - 1 && t == geo.tiles(o) - 1 && threadIdx.x < geo.rem) {
-    const int64_t j = 4 * geo.n4 + threadIdx.x;
+  if (r.tail && threadIdx.x < p.rem) {
+    const int64_t j = 4 * p.n4 + threadIdx.x;
+    const int64_t so = p.n4 - slo;
     const float mine = local_partial1<M>(p, j);
-    float s = p.me == 0 ? mine : p.src[0][j];
-    for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == p.me ? mine : p.src[d][j]);
-    store_members1<M>(p, j, __fdiv_rn(s, kf));
+    float s = o == 0 ? mine : stage[stage_off(p, 0, so) + threadIdx.x];
+    for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == o ? mine : stage[stage_off(p, d, so) + threadIdx.x]);
+    const float xbar = __fdiv_rn(s, kf);
+    for (int m = 0; m < p.m; ++m) p.x[m][j] = xbar;
+    for (int d = 0; d < p.kp; ++d)
+      if (d != o) p.xfirst[d][j] = xbar;
   }
 }
 
 template <int M, int U>
-__device__ void tile_C(const XPart& p, const Geo<U>& geo, int o, int64_t t) {
-  const int64_t lo = geo.lo(o), hi = geo.hi(o);
-  const int64_t i0 = lo + t * kXThreads * U;
-  float4 v[U];
+__device__ void item_C(const XPart& p, int o, int64_t c) {
+  if (p.m == 1) return;  // the owner stored xbar straight into my only replica
+  const ChunkRange r = chunk_range(p, o, c);
+  for (int64_t t0 = r.lo; t0 < r.hi; t0 += kXThreads * U) {
+    float4 v[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = i0 + u * kXThreads + threadIdx.x;
-    if (i < hi) v[u] = ldv(p.src[o] + 4 * i);  // NVLink
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = i0 + u * kXThreads + threadIdx.x;
-    if (i < hi) store_members4<M>(p, i, v[u]);
-  }
-  if (o == geo.kp - 1 && t == geo.tiles(o) - 1 && threadIdx.x < geo.rem) {
-    const int64_t j = 4 * geo.n4 + threadIdx.x;
-    store_members1<M>(p, j, p.src[o][j]);
-  }
-}
-
-// Map the t-th tile of part p's A (or C) range to (slice o != me, tile within slice).
-template <int U>
-__device__ __forceinline__ void other_slice_tile(const XPart& p, const Geo<U>& geo, int64_t t, int* o_out,
-                                                 int64_t* t_out) {
-  for (int o = 0; o < p.kp; ++o) {
-    if (o == p.me) continue;
-    const int64_t n = geo.tiles(o);
-    if (t < n) {
-      *o_out = o;
-      *t_out = t;
-      return;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) v[u] = ldv(p.x[0] + 4 * i);
     }
-    t -= n;
-  }
-  *o_out = -1;
-  *t_out = 0;
-}
-
-__device__ void signal_peers(const XTask& T, const XPart& p, int phase) {
-  __threadfence_system();
-  for (int d = 0; d < p.kp; ++d)
-    if (d != p.me) st_release_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, phase), p.tag);
-}
-
-__device__ void wait_peer(const XTask& T, const XPart& p, int d, int phase) {
-  const unsigned long long* f = flag_at(T.my_flags, p.slot, p.gpu[d], phase);
-  while (ld_acquire_sys(f) != p.tag) __nanosleep(64);
-}
-
-// Add this CTA's finished tiles of (part, phase) to the phase counter; the CTA
-// that completes the phase signals every peer.
-__device__ void flush_count(const XTask& T, int pi, int phase, int64_t mine, int64_t total) {
-  if (mine == 0) return;
-  const XPart& p = T.part[pi];
-  __threadfence();
-  unsigned long long* c = T.my_counters + static_cast<int64_t>(p.slot) * kFlagPhases + phase;
-  const unsigned long long before = atomicAdd(c, static_cast<unsigned long long>(mine));
-  if (before + mine == static_cast<unsigned long long>(total)) {
-    atomicExch(c, 0ull);
-    signal_peers(T, p, phase);
-  }
-}
-
-// Counters per part: A tiles -> A-done ("my partials are ready"); B tiles -> B-done
-// ("my slice's means are ready"); B and C tiles -> C-done ("I have finished
-// reading every peer's memory for this group"), the condition for peers to end.
-__device__ void publish(const XTask& T, int region, const int64_t* cnt) {
-  for (int pi = 0; pi < T.nparts; ++pi) {
-    const XPart& p = T.part[pi];
-    if (region == 0) {
-      flush_count(T, pi, kPhaseA, cnt[pi], p.ta);
-    } else {
-      if (region == 1) flush_count(T, pi, kPhaseB, cnt[pi], p.tb);
-      flush_count(T, pi, kPhaseC, cnt[pi], p.tb + p.ta);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) {
+#pragma unroll
+        for (int m = 1; m < M; ++m)
+          if (m < p.m) stv(p.x[m] + 4 * i, v[u]);
+      }
     }
   }
+  if (r.tail && threadIdx.x < p.rem) {
+    const int64_t j = 4 * p.n4 + threadIdx.x;
+    const float v = p.x[0][j];
+    for (int m = 1; m < p.m; ++m) p.x[m][j] = v;
+  }
+}
+
+// item index within an A or C range of part p -> (slice o != me, chunk c), chunk-major
+__device__ __forceinline__ void other_item(const XPart& p, int64_t i, int* o, int64_t* c) {
+  const int j = static_cast<int>(i % (p.kp - 1));
+  *c = i / (p.kp - 1);
+  *o = j < p.me ? j : j + 1;
 }
 
 // M bounds the local member count of every part (register budget).
 template <int M, int U>
 __global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
-  // Phases with no tiles anywhere are complete from the start.
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // READY: my staging is free for these groups (my previous kernel has finished)
     for (int pi = 0; pi < T.nparts; ++pi) {
       const XPart& p = T.part[pi];
-      if (p.ta == 0) signal_peers(T, p, kPhaseA);
-      if (p.tb == 0) signal_peers(T, p, kPhaseB);
-      // C-done needs B + C tiles, and ta + tb >= 1 whenever n >= 1
+      for (int d = 0; d < p.kp; ++d)
+        if (d != p.me) st_release_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagReady, 0), p.tag);
     }
   }
-  int64_t cnt[kMaxXParts];
-  uint32_t confirmed[kMaxXParts];  // bit d: A-done of GPU index d seen; bit 8+o: B-done of owner o seen
-#pragma unroll
-  for (int pi = 0; pi < kMaxXParts; ++pi) {
-    cnt[pi] = 0;
-    confirmed[pi] = 0;
-  }
-  int region = 0;  // 0 = A, 1 = B, 2 = C
-  const int64_t total = T.c_end;
-  for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
-    const int r = q < T.b_begin ? 0 : (q < T.c_begin ? 1 : 2);
-    while (region < r) {  // leaving a region: publish this CTA's tile counts for it
-      __syncthreads();
-      if (threadIdx.x == 0) publish(T, region, cnt);
-#pragma unroll
-      for (int pi = 0; pi < kMaxXParts; ++pi) cnt[pi] = 0;
-      ++region;
-    }
-    // locate (part, tile) in the region
-    const int64_t base = r == 0 ? 0 : (r == 1 ? T.b_begin : T.c_begin);
-    int64_t t = q - base;
+  uint32_t ready_seen = 0;  // bit 8*pi + o: READY of part pi's owner o observed (thread 0)
+  for (int64_t q = blockIdx.x; q < T.total_items; q += gridDim.x) {
+    const int region = q < T.b_begin ? 0 : (q < T.c_begin ? 1 : 2);
+    int64_t t = q - (region == 0 ? 0 : (region == 1 ? T.b_begin : T.c_begin));
     int pi = 0;
-    for (; pi < T.nparts; ++pi) {
-      const int64_t n = r == 1 ? T.part[pi].tb : T.part[pi].ta;
+    for (; pi < T.nparts - 1; ++pi) {
+      const XPart& pp = T.part[pi];
+      const int64_t n = region == 1 ? pp.nch : static_cast<int64_t>(pp.kp - 1) * pp.nch;
       if (t < n) break;
       t -= n;
     }
     const XPart& p = T.part[pi];
-    Geo<U> geo{p.n4, p.S4, p.rem, p.kp};
-    if (r == 0) {
+    if (region == 0) {
       int o;
-      int64_t tt;
-      other_slice_tile(p, geo, t, &o, &tt);
-      tile_A<M, U>(p, geo, o, tt);
-    } else if (r == 1) {
-      if (threadIdx.x == 0)
-        for (int d = 0; d < p.kp; ++d)
-          if (d != p.me && !((confirmed[pi] >> d) & 1)) {
-            wait_peer(T, p, d, kPhaseA);
-            confirmed[pi] |= 1u << d;
-          }
-      __syncthreads();
-      tile_B<M, U>(p, geo, t);
-    } else {
-      int o;
-      int64_t tt;
-      other_slice_tile(p, geo, t, &o, &tt);
-      if (threadIdx.x == 0 && !((confirmed[pi] >> (8 + o)) & 1)) {
-        wait_peer(T, p, o, kPhaseB);
-        confirmed[pi] |= 1u << (8 + o);
+      int64_t c;
+      other_item(p, t, &o, &c);
+      const uint32_t bit = 1u << (8 * (pi & 3) + o);
+      if (threadIdx.x == 0 && (pi >= 4 || !(ready_seen & bit))) {
+        wait_flag(flag_at(T.my_flags, p.slot, p.gpu[o], kFlagReady, 0), p.tag);
+        if (pi < 4) ready_seen |= bit;
       }
       __syncthreads();
-      tile_C<M, U>(p, geo, o, tt);
+      item_A<M, U>(p, o, c);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        st_release_sys(flag_at(p.pflags[o], p.slot, T.my_gpu, kFlagA, c), p.tag);
+      }
+    } else if (region == 1) {
+      if (threadIdx.x == 0)
+        for (int d = 0; d < p.kp; ++d)
+          if (d != p.me) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, t), p.tag);
+      __syncthreads();
+      item_B<M, U>(p, t);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int d = 0; d < p.kp; ++d)
+          if (d != p.me) st_release_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagB, t), p.tag);
+      }
+    } else {
+      int o;
+      int64_t c;
+      other_item(p, t, &o, &c);
+      if (threadIdx.x == 0) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[o], kFlagB, c), p.tag);
+      __syncthreads();
+      item_C<M, U>(p, o, c);
     }
-    cnt[pi] += 1;
-  }
-  // publish the remaining regions (a CTA may end inside A or B)
-  while (region < 3) {
     __syncthreads();
-    if (threadIdx.x == 0) publish(T, region, cnt);
-#pragma unroll
-    for (int pi = 0; pi < kMaxXParts; ++pi) cnt[pi] = 0;
-    ++region;
   }
-  // end of the group: wait until every peer has finished reading my memory
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int pi = 0; pi < T.nparts; ++pi)
-      for (int d = 0; d < T.part[pi].kp; ++d)
-        if (d != T.part[pi].me) wait_peer(T, T.part[pi], d, kPhaseC);
 }
 
 int g_sms = 0;
+
+// Tuning knobs (read once): RP_XGPU_U (1|2|4 float4 per thread and tile row),
+// RP_XGPU_CTAS_PER_SM (cap on resident CTAs used), RP_XGPU_CHUNK_F4 (min chunk).
+int env_int(const char* name, int def) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : def;
+}
+int g_u = -1, g_cps = -1;
+int64_t g_min_chunk = -1;
 
 template <int M, int U>
 int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
@@ -374,34 +339,18 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sms <= 0) g_sms = 148;
   }
-  // tile geometry per part
   int64_t a = 0, b = 0;
-  const int64_t tile = static_cast<int64_t>(kXThreads) * U;
   for (int pi = 0; pi < T.nparts; ++pi) {
     XPart& p = T.part[pi];
-    p.n4 = T.n / 4;
-    p.rem = static_cast<int32_t>(T.n - 4 * p.n4);
-    p.S4 = ((p.n4 + p.kp - 1) / p.kp + tile - 1) / tile * tile;
-    int64_t ta = 0, tb = 0;
-    for (int o = 0; o < p.kp; ++o) {
-      const int64_t lo = std::min(o * p.S4, p.n4), hi = std::min((o + 1) * p.S4, p.n4);
-      int64_t t = (hi - lo + tile - 1) / tile;
-      if (o == p.kp - 1 && p.rem > 0 && (hi - lo) % tile == 0) ++t;
-      if (o == p.me)
-        tb = t;
-      else
-        ta += t;
-    }
-    p.ta = ta;
-    p.tb = tb;
-    a += ta;
-    b += tb;
+    a += static_cast<int64_t>(p.kp - 1) * p.nch;
+    b += p.nch;
   }
   T.b_begin = a;
   T.c_begin = a + b;
-  T.c_end = a + b + a;
-  const int64_t cap = static_cast<int64_t>(g_sms) * occ;  // all CTAs co-resident
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.c_end)));
+  T.total_items = a + b + a;
+  int64_t cap = static_cast<int64_t>(g_sms) * occ;  // all CTAs co-resident
+  if (g_cps > 0) cap = std::min<int64_t>(cap, static_cast<int64_t>(g_sms) * g_cps);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.total_items)));
   xgpu_kernel<M, U><<<blocks, kXThreads, 0, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -411,7 +360,24 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   return RP_OK;
 }
 
+constexpr int64_t kTileF4 = static_cast<int64_t>(kXThreads) * 4;  // slice/chunk boundaries: multiples of every U
+
 }  // namespace
+
+void xgpu_geometry(XPart& p, int64_t n) {
+  p.n4 = n / 4;
+  p.rem = static_cast<int32_t>(n - 4 * p.n4);
+  p.S4 = ((p.n4 + p.kp - 1) / p.kp + kTileF4 - 1) / kTileF4 * kTileF4;
+  if (g_min_chunk < 0) g_min_chunk = env_int("RP_XGPU_CHUNK_F4", static_cast<int>(kMinChunkF4));
+  int64_t ch = std::max<int64_t>((p.S4 + kMaxChunks - 1) / kMaxChunks, g_min_chunk);
+  p.CH = (ch + kTileF4 - 1) / kTileF4 * kTileF4;
+  p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
+}
+
+int64_t xgpu_stage_region_bytes(int64_t n) {
+  // kp rows of (S4 + 1) float4, S4 <= n4/kp + tile: at most 4n + 16 * kp * (tile + 2)
+  return 4 * n + 16LL * kMaxXGpus * (kTileF4 + 2);
+}
 
 int launch_xgpu(XTask& T, void* stream, std::string* err) {
   if (T.nparts < 1 || T.nparts > kMaxXParts) {
@@ -421,22 +387,28 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   int mmax = 0;
   for (int pi = 0; pi < T.nparts; ++pi) {
     const XPart& p = T.part[pi];
-    if (p.m < 1 || p.m > kMaxXLocal || p.kp < 2 || p.kp > kMaxXGpus || p.me < 0 || p.me >= p.kp) {
+    if (p.m < 1 || p.m > kMaxXLocal || p.kp < 2 || p.kp > kMaxXGpus || p.me < 0 || p.me >= p.kp ||
+        p.nch < 1 || p.nch > kMaxChunks) {
       *err = "xgpu: bad part descriptor";
       return RP_EINVAL;
     }
     for (int d = 0; d < p.kp; ++d)
-      if (!p.src[d] || !p.pflags[d] || (reinterpret_cast<uintptr_t>(p.src[d]) & 15)) {
+      if (!p.stage[d] || !p.xfirst[d] || !p.pflags[d] || (reinterpret_cast<uintptr_t>(p.xfirst[d]) & 15) ||
+          (reinterpret_cast<uintptr_t>(p.stage[d]) & 15)) {
         *err = "xgpu: peer pointers missing (call rp_peer_import) or misaligned";
         return RP_EINVAL;
       }
     mmax = std::max(mmax, p.m);
   }
-  // every cross part of a step must be in ONE launch (two launches on one stream
-  // could wait on each other across GPUs), so M is the largest local count
+  // every cross part of a step is in ONE launch (two launches on one stream could
+  // wait on each other across GPUs), so M is the largest local member count
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (mmax <= 1) return launch_m<1, 2>(T, s, err);
-  if (mmax <= 2) return launch_m<2, 2>(T, s, err);
+  if (g_u < 0) {
+    g_u = env_int("RP_XGPU_U", 2);
+    g_cps = env_int("RP_XGPU_CTAS_PER_SM", 0);
+  }
+  if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4>(T, s, err) : (g_u == 1 ? launch_m<1, 1>(T, s, err) : launch_m<1, 2>(T, s, err));
+  if (mmax <= 2) return g_u >= 4 ? launch_m<2, 4>(T, s, err) : (g_u == 1 ? launch_m<2, 1>(T, s, err) : launch_m<2, 2>(T, s, err));
   if (mmax <= 4) return launch_m<4, 1>(T, s, err);
   return launch_m<8, 1>(T, s, err);
 }

@@ -107,6 +107,9 @@ class rp_peer_info(ctypes.Structure):
         ("pid", ctypes.c_int32),
         ("flags_handle", ctypes.c_uint8 * RP_IPC_HANDLE_BYTES),
         ("flags_offset", ctypes.c_int64),
+        ("stage_handle", ctypes.c_uint8 * RP_IPC_HANDLE_BYTES),
+        ("stage_offset", ctypes.c_int64),
+        ("stage_region_bytes", ctypes.c_int64),
         ("x_handle", (ctypes.c_uint8 * RP_IPC_HANDLE_BYTES) * RP_MAX_LOCAL),
         ("x_offset", ctypes.c_int64 * RP_MAX_LOCAL),
     ]
