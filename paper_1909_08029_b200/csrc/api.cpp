@@ -17,6 +17,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -128,6 +129,10 @@ struct rp_ctx {
   float* peer_x[RP_MAX_WORLD] = {};                 // replicas of remote workers, mapped
   unsigned long long* peer_flags[RP_MAX_GPUS] = {};  // flag arrays of the other GPUs, mapped
   float* peer_stage[RP_MAX_GPUS] = {};              // staging buffers of the other GPUs, mapped
+  // optional cross-kernel item timeline (env RP_XGPU_PROFILE=path): last launch only
+  rp::XItemRecord* prof = nullptr;
+  int64_t prof_cap = 0, prof_items = 0;
+  std::string prof_path;
   std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
 };
 
@@ -194,7 +199,8 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // local (caller holds mu). The kernel runs on the stream of the lowest local
 // member after every member's arrival event; every member's stream is then
 // ordered after the kernel and records its own completion event.
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream);
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
+                 cudaStream_t stream);
 
 int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (all_seqs.empty()) return RP_OK;
@@ -213,8 +219,16 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   WorkerSlot& L = c->w[launcher];
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if (((all >> m) & 1) && m != launcher) CUDA_TRY(cudaStreamWaitEvent(L.stream, c->w[m].ev_arrive, 0));
-  // One fused launch for all ready groups (chunked at kMaxTasks groups /
-  // kMaxTaskMembers members).
+  // With cross-GPU groups in the batch, intra-GPU groups of <= 4 members ride in
+  // the same launch (their HBM work overlaps the NVLink transfers).
+  std::vector<int64_t> fused;
+  if (!cross.empty()) {
+    bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
+    for (int64_t q : seqs) ok = ok && c->active.at(q).g.size <= rp::kMaxFusedK;
+    if (ok) fused.swap(seqs);
+  }
+  // One fused launch for all remaining intra-GPU groups (chunked at kMaxTasks
+  // groups / kMaxTaskMembers members).
   size_t gi = 0;
   while (gi < seqs.size()) {
     rp::MultiTask t{};
@@ -256,7 +270,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     c->stats.bytes_hbm += bytes;
   }
   if (!cross.empty()) {
-    const int rc = launch_cross(c, cross, L.stream);
+    const int rc = launch_cross(c, cross, fused, L.stream);
     if (rc != RP_OK) return rc;
   }
   CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
@@ -274,7 +288,8 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
 
 // This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch
 // (caller holds mu; members' arrival events already joined into `stream`).
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream) {
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
+                 cudaStream_t stream) {
   if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
   if (static_cast<int>(seqs.size()) > rp::kMaxXParts)
     return fail(RP_EINVAL, "more than 8 cross-GPU groups on one GPU in one step");
@@ -324,6 +339,20 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
     c->stats.groups_launched++;
     c->stats.cross_gpu_groups++;
   }
+  int64_t hbm_local = 0;
+  for (int64_t q : local) {  // fused intra-GPU groups (L items)
+    ActiveGroup& a = c->active.at(q);
+    rp::XLocalGroup& G = T.lg[T.nlocal++];
+    G.k = a.g.size;
+    for (int i = 0; i < a.g.size; ++i) {
+      G.x[i] = c->w[a.g.members[i]].x;
+      G.g[i] = a.grad[i];
+      G.lr[i] = a.lr[i];
+      hbm_local += (a.grad[i] ? 12 : 8) * T.n;
+    }
+    c->stats.groups_launched++;
+    if (a.g.size == 1) c->stats.singleton_groups++;
+  }
   const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timing) {
@@ -331,6 +360,21 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
     e1 = timing_event(c);
     if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
     CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  if (!c->prof_path.empty()) {
+    int64_t items = 0;
+    // upper bound: chunks per slice <= kMaxChunks, per local group <= resident CTAs + 1
+    for (int pi = 0; pi < T.nparts; ++pi) items += (2 * T.part[pi].kp - 1) * static_cast<int64_t>(rp::kMaxChunks);
+    items += static_cast<int64_t>(T.nlocal) * 4096;
+    if (items > c->prof_cap) {
+      if (c->prof) cudaFree(c->prof);
+      c->prof = nullptr;
+      c->prof_cap = 0;
+      if (cudaMalloc(&c->prof, items * sizeof(rp::XItemRecord)) == cudaSuccess) c->prof_cap = items;
+    }
+    T.prof = c->prof;
+    c->prof_items = items;
+    if (c->prof) cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
   }
   std::string err;
   const int rc = rp::launch_xgpu(T, stream, &err);
@@ -350,6 +394,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t strea
     // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
     hbm += rd * T.n + 4 * (p.kp - 1) * mine + 4 * p.m * mine + 8 * (p.m - 1) * others;
   }
+  hbm += hbm_local;
   if (timing) {
     CUDA_TRY(cudaEventRecord(e1, stream));
     c->timed.push_back({e0, e1, hbm, nvl, true});
@@ -450,6 +495,7 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       s.own_stream = true;
     }
     if (k.n_gpus > 1) {
+      if (const char* pp = std::getenv("RP_XGPU_PROFILE")) c->prof_path = pp;
       if (wpg > RP_MAX_LOCAL) {
         rp_finalize(c);
         return fail(RP_EINVAL, "rp_init: at most 16 workers per GPU in a multi-GPU job");
@@ -564,6 +610,18 @@ int rp_finalize(rp_ctx* c) {
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (c->flags) cudaFree(c->flags);
     if (c->stage) cudaFree(c->stage);
+    if (c->prof) {
+      // dump the item timeline of the last cross-GPU launch
+      std::vector<rp::XItemRecord> h(c->prof_items);
+      if (cudaMemcpy(h.data(), c->prof, h.size() * sizeof(rp::XItemRecord), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        const std::string path = c->prof_path + "." + std::to_string(c->cfg.rank);
+        if (FILE* f = std::fopen(path.c_str(), "wb")) {
+          std::fwrite(h.data(), sizeof(rp::XItemRecord), h.size(), f);
+          std::fclose(f);
+        }
+      }
+      cudaFree(c->prof);
+    }
     for (auto& s : c->w) {
       if (s.stream) cudaStreamSynchronize(s.stream);
       if (s.ev_arrive) cudaEventDestroy(s.ev_arrive);

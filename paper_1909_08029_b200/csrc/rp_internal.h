@@ -74,8 +74,8 @@ constexpr int kMaxXLocal = 8;    // local members of one cross-GPU group
 constexpr int kMaxXGpus = 8;     // GPUs of one group
 constexpr int kFlagSlots = 64;   // slot = lowest member of the group
 constexpr int kFlagSrc = 8;      // source GPU
-constexpr int kMaxChunks = 1024; // chunks per owner slice
-constexpr int64_t kMinChunkF4 = 2048;  // 32 KiB per buffer and chunk
+constexpr int kMaxChunks = 4096; // chunks per owner slice
+constexpr int64_t kMinChunkF4 = 8192;  // 128 KiB per buffer and chunk (fence amortization)
 constexpr int kFlagA = 0, kFlagB = 1, kFlagReady = 2;
 constexpr int64_t kFlagStride = 2 * kMaxChunks + 1;  // A[chunk], B[chunk], READY
 constexpr size_t kFlagWords = static_cast<size_t>(kFlagSlots) * kFlagSrc * kFlagStride;
@@ -98,12 +98,37 @@ struct XPart {
   int32_t gpu[kMaxXGpus];                 // GPU ids, ascending
 };
 
+// Optional per-item timeline (RP_XGPU_PROFILE): 4 x u64 per item.
+struct XItemRecord {
+  unsigned long long t_start, t_ready, t_end;  // %globaltimer ns: begin, wait satisfied, flag posted
+  unsigned long long meta;                     // kind (2 bits) | part (6) | cta (24) | chunk (32)
+};
+
+// Intra-GPU groups of the same step fused into the cross-GPU launch ("L items"),
+// so their HBM-only work overlaps the NVLink transfers.
+constexpr int kMaxXLocalGroups = 16;
+constexpr int kMaxFusedK = 4;
+struct XLocalGroup {
+  int32_t k;
+  float* x[kMaxFusedK];
+  const float* g[kMaxFusedK];
+  float lr[kMaxFusedK];
+};
+
+// Kernel parameters exceed 4 KB: CUDA >= 12.1 large-parameter launches (sm_70+).
 struct XTask {
   int32_t nparts;
   int32_t my_gpu;
   int64_t n;
-  int64_t b_begin, c_begin, total_items;   // work-item ranges (filled by the launcher)
+  // work items (filled by the launcher): items[q] = kind << 30 | part << 27 | index,
+  // ordered so that B items of chunk c come one CTA round after its A items
+  const uint32_t* items;
+  int64_t total_items;
+  int64_t chl, nchl;                       // L items: chunk (float4) and chunks per local group
   unsigned long long* my_flags;
+  XItemRecord* prof;                       // nullptr unless profiling; indexed by item
+  int32_t nlocal;
+  XLocalGroup lg[kMaxXLocalGroups];
   XPart part[kMaxXParts];
 };
 

@@ -38,8 +38,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "rp_internal.h"
 
@@ -48,6 +52,7 @@ namespace rp {
 namespace {
 
 constexpr int kXThreads = 256;
+constexpr int64_t kTileF4 = static_cast<int64_t>(kXThreads) * 4;  // slice/chunk boundaries: multiples of every U
 
 __device__ __forceinline__ float4 ldv(const float* p) {
   float4 v;
@@ -245,6 +250,59 @@ __device__ void item_C(const XPart& p, int o, int64_t c) {
   }
 }
 
+// L item: chunk c of fused intra-GPU group gi (alg1 steps 2+4 on one GPU, pinned fold)
+template <int K, int U>
+__device__ void item_L_k(const XLocalGroup& G, int64_t lo, int64_t hi, bool tail, int64_t n4, int rem) {
+  for (int64_t t0 = lo; t0 < hi; t0 += kXThreads * U) {
+    float4 xv[U][K], gv[U][K];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < hi)
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+          xv[u][m] = ldv(G.x[m] + 4 * i);
+          if (G.g[m]) gv[u][m] = ldg_nc(G.g[m] + 4 * i);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < hi) {
+        float4 s = G.g[0] ? sgd4(xv[u][0], gv[u][0], G.lr[0]) : xv[u][0];
+#pragma unroll
+        for (int m = 1; m < K; ++m) s = add4(s, G.g[m] ? sgd4(xv[u][m], gv[u][m], G.lr[m]) : xv[u][m]);
+        if (K > 1) s = div4(s, static_cast<float>(K));
+#pragma unroll
+        for (int m = 0; m < K; ++m) stv(G.x[m] + 4 * i, s);
+      }
+    }
+  }
+  if (tail && threadIdx.x < rem) {
+    const int64_t j = 4 * n4 + threadIdx.x;
+    float s = G.g[0] ? sgd1(G.x[0][j], G.g[0][j], G.lr[0]) : G.x[0][j];
+    for (int m = 1; m < K; ++m) s = __fadd_rn(s, G.g[m] ? sgd1(G.x[m][j], G.g[m][j], G.lr[m]) : G.x[m][j]);
+    if (K > 1) s = __fdiv_rn(s, static_cast<float>(K));
+    for (int m = 0; m < K; ++m) G.x[m][j] = s;
+  }
+}
+
+template <int U>
+__device__ void item_L(const XTask& T, int64_t idx) {
+  const XLocalGroup& G = T.lg[idx / T.nchl];
+  const int64_t c = idx % T.nchl;
+  const int64_t n4 = T.n / 4;
+  const int rem = static_cast<int>(T.n - 4 * n4);
+  const int64_t lo = min(c * T.chl, n4), hi = min((c + 1) * T.chl, n4);
+  const bool tail = (c == T.nchl - 1) && rem > 0;
+  switch (G.k) {
+    case 1: item_L_k<1, U>(G, lo, hi, tail, n4, rem); break;
+    case 2: item_L_k<2, U>(G, lo, hi, tail, n4, rem); break;
+    case 3: item_L_k<3, U>(G, lo, hi, tail, n4, rem); break;
+    default: item_L_k<4, U>(G, lo, hi, tail, n4, rem); break;
+  }
+}
+
 // item index within an A or C range of part p -> (slice o != me, chunk c), chunk-major
 __device__ __forceinline__ void other_item(const XPart& p, int64_t i, int* o, int64_t* c) {
   const int j = static_cast<int>(i % (p.kp - 1));
@@ -252,9 +310,15 @@ __device__ __forceinline__ void other_item(const XPart& p, int64_t i, int* o, in
   *o = j < p.me ? j : j + 1;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // M bounds the local member count of every part (register budget).
 template <int M, int U>
-__global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
+__global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // READY: my staging is free for these groups (my previous kernel has finished)
     for (int pi = 0; pi < T.nparts; ++pi) {
@@ -265,14 +329,25 @@ __global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
   }
   uint32_t ready_seen = 0;  // bit 8*pi + o: READY of part pi's owner o observed (thread 0)
   for (int64_t q = blockIdx.x; q < T.total_items; q += gridDim.x) {
-    const int region = q < T.b_begin ? 0 : (q < T.c_begin ? 1 : 2);
-    int64_t t = q - (region == 0 ? 0 : (region == 1 ? T.b_begin : T.c_begin));
-    int pi = 0;
-    for (; pi < T.nparts - 1; ++pi) {
-      const XPart& pp = T.part[pi];
-      const int64_t n = region == 1 ? pp.nch : static_cast<int64_t>(pp.kp - 1) * pp.nch;
-      if (t < n) break;
-      t -= n;
+    const uint32_t it = T.items[q];
+    const int region = static_cast<int>(it >> 30);  // 0 = A, 1 = B, 2 = C, 3 = L
+    const int pi = static_cast<int>((it >> 27) & 7);
+    int64_t t = static_cast<int64_t>(it & ((1u << 27) - 1));
+    unsigned long long ts = 0, tr = 0;
+    if (T.prof && threadIdx.x == 0) ts = gtimer();
+    if (region == 3) {
+      if (T.prof && threadIdx.x == 0) tr = gtimer();
+      item_L<1>(T, t);
+      if (T.prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          XItemRecord rec{ts, tr, gtimer(),
+                          (3ull << 62) | (static_cast<unsigned long long>(blockIdx.x & 0xFFFFFF) << 32) |
+                              static_cast<unsigned long long>(t)};
+          T.prof[q] = rec;
+        }
+      }
+      continue;
     }
     const XPart& p = T.part[pi];
     if (region == 0) {
@@ -285,6 +360,7 @@ __global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
         if (pi < 4) ready_seen |= bit;
       }
       __syncthreads();
+      if (T.prof && threadIdx.x == 0) tr = gtimer();
       item_A<M, U>(p, o, c);
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -296,7 +372,8 @@ __global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
         for (int d = 0; d < p.kp; ++d)
           if (d != p.me) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, t), p.tag);
       __syncthreads();
-      item_B<M, U>(p, t);
+      if (T.prof && threadIdx.x == 0) tr = gtimer();
+      item_B<M, 1>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -309,13 +386,81 @@ __global__ void __launch_bounds__(kXThreads) xgpu_kernel(const XTask T) {
       other_item(p, t, &o, &c);
       if (threadIdx.x == 0) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[o], kFlagB, c), p.tag);
       __syncthreads();
+      if (T.prof && threadIdx.x == 0) tr = gtimer();
       item_C<M, U>(p, o, c);
     }
     __syncthreads();
+    if (T.prof && threadIdx.x == 0) {
+      XItemRecord rec;
+      rec.t_start = ts;
+      rec.t_ready = tr;
+      rec.t_end = gtimer();
+      rec.meta = (static_cast<unsigned long long>(region) << 62) | (static_cast<unsigned long long>(pi) << 56) |
+                 (static_cast<unsigned long long>(blockIdx.x & 0xFFFFFF) << 32) | static_cast<unsigned long long>(t);
+      T.prof[q] = rec;
+    }
   }
 }
 
 int g_sms = 0;
+
+// Host-built work-item order, cached per launch shape. Virtual time in units of a
+// part's chunks: A(o, c) at c, B(c) at c + lag, C(o, c) at c + 2 lag; L items spread
+// evenly over the A and B items. The default lag = nch runs all A items, then all B
+// items (chunk-pipelined lags were slower on 2 B200: more, smaller chunks pay more
+// system fences; profiles/r01_xgpu_lag_sweep_2gpu.txt).
+int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count, std::string* err) {
+  static std::mutex mu;
+  static std::map<std::string, std::pair<uint32_t*, int64_t>> cache;
+  std::string key = std::to_string(T.my_gpu) + "/" + std::to_string(ctas) + "/" + std::to_string(T.nlocal) + "/" +
+                    std::to_string(T.nchl);
+  for (int pi = 0; pi < T.nparts; ++pi)
+    key += "/" + std::to_string(T.part[pi].kp) + "," + std::to_string(T.part[pi].me) + "," +
+           std::to_string(T.part[pi].nch);
+  std::lock_guard<std::mutex> lk(mu);
+  auto hit = cache.find(key);
+  if (hit != cache.end()) {
+    *out = hit->second.first;
+    *count = hit->second.second;
+    return RP_OK;
+  }
+  struct Ent {
+    double t;
+    int order;
+    uint32_t code;
+  };
+  std::vector<Ent> v;
+  double tmax = 1.0;
+  for (int pi = 0; pi < T.nparts; ++pi) {
+    const XPart& p = T.part[pi];
+    const double nch = static_cast<double>(p.nch);
+    // lag: RP_XGPU_LAG (chunks) or, by default, all A items before any B item
+    const double lag = g_lag > 0 ? std::min<double>(nch, g_lag) : nch;
+    const uint32_t P = static_cast<uint32_t>(pi) << 27;
+    for (int64_t i = 0; i < (p.kp - 1) * p.nch; ++i) {
+      const double c = static_cast<double>(i / (p.kp - 1));
+      v.push_back({c / nch, 0, (0u << 30) | P | static_cast<uint32_t>(i)});
+      v.push_back({(c + 2 * lag) / nch, 2, (2u << 30) | P | static_cast<uint32_t>(i)});
+    }
+    for (int64_t c = 0; c < p.nch; ++c) v.push_back({(c + lag) / nch, 1, (1u << 30) | P | static_cast<uint32_t>(c)});
+    tmax = std::max(tmax, (nch + lag) / nch);
+  }
+  const int64_t nl = static_cast<int64_t>(T.nlocal) * T.nchl;
+  for (int64_t l = 0; l < nl; ++l) v.push_back({tmax * static_cast<double>(l) / nl, 3, (3u << 30) | static_cast<uint32_t>(l)});
+  std::stable_sort(v.begin(), v.end(), [](const Ent& a, const Ent& b) { return a.t < b.t || (a.t == b.t && a.order < b.order); });
+  std::vector<uint32_t> h(v.size());
+  for (size_t i = 0; i < v.size(); ++i) h[i] = v[i].code;
+  uint32_t* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemcpy(d, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    *err = "xgpu: item list upload failed";
+    return RP_ECUDA;
+  }
+  cache[key] = {d, static_cast<int64_t>(h.size())};
+  *out = d;
+  *count = static_cast<int64_t>(h.size());
+  return RP_OK;
+}
 
 // Tuning knobs (read once): RP_XGPU_U (1|2|4 float4 per thread and tile row),
 // RP_XGPU_CTAS_PER_SM (cap on resident CTAs used), RP_XGPU_CHUNK_F4 (min chunk).
@@ -323,7 +468,7 @@ int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : def;
 }
-int g_u = -1, g_cps = -1;
+int g_u = -1, g_cps = -1, g_lag = -1;
 int64_t g_min_chunk = -1;
 
 template <int M, int U>
@@ -339,17 +484,25 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sms <= 0) g_sms = 148;
   }
-  int64_t a = 0, b = 0;
-  for (int pi = 0; pi < T.nparts; ++pi) {
-    XPart& p = T.part[pi];
-    a += static_cast<int64_t>(p.kp - 1) * p.nch;
-    b += p.nch;
-  }
-  T.b_begin = a;
-  T.c_begin = a + b;
-  T.total_items = a + b + a;
   int64_t cap = static_cast<int64_t>(g_sms) * occ;  // all CTAs co-resident
   if (g_cps > 0) cap = std::min<int64_t>(cap, static_cast<int64_t>(g_sms) * g_cps);
+  if (g_min_chunk < 0) g_min_chunk = env_int("RP_XGPU_CHUNK_F4", static_cast<int>(kMinChunkF4));
+  for (int pi = 0; pi < T.nparts; ++pi) {
+    XPart& p = T.part[pi];
+    // chunk: about one A and one B item per resident CTA (each CTA pays the system fence
+    // behind a flag about twice per group: measured best on 2 B200, profiles/r01_xgpu_*),
+    // at least g_min_chunk float4, at most kMaxChunks chunks per slice
+    int64_t ch = std::max<int64_t>({(p.S4 + cap - 1) / cap, g_min_chunk, (p.S4 + kMaxChunks - 1) / kMaxChunks});
+    p.CH = (ch + kTileF4 - 1) / kTileF4 * kTileF4;
+    p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
+  }
+  const int64_t n4 = T.n / 4;
+  T.chl = std::max<int64_t>(kTileF4, (std::max<int64_t>(n4, 1) * T.nlocal / std::max<int64_t>(cap, 1) + kTileF4 - 1) /
+                                         kTileF4 * kTileF4);
+  T.chl = std::max<int64_t>(T.chl, g_min_chunk / kTileF4 * kTileF4);
+  T.nchl = std::max<int64_t>(1, (n4 + T.chl - 1) / T.chl);
+  const int rc = item_list(T, cap, &T.items, &T.total_items, err);
+  if (rc != RP_OK) return rc;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.total_items)));
   xgpu_kernel<M, U><<<blocks, kXThreads, 0, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
@@ -360,18 +513,14 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   return RP_OK;
 }
 
-constexpr int64_t kTileF4 = static_cast<int64_t>(kXThreads) * 4;  // slice/chunk boundaries: multiples of every U
-
 }  // namespace
 
 void xgpu_geometry(XPart& p, int64_t n) {
   p.n4 = n / 4;
   p.rem = static_cast<int32_t>(n - 4 * p.n4);
   p.S4 = ((p.n4 + p.kp - 1) / p.kp + kTileF4 - 1) / kTileF4 * kTileF4;
-  if (g_min_chunk < 0) g_min_chunk = env_int("RP_XGPU_CHUNK_F4", static_cast<int>(kMinChunkF4));
-  int64_t ch = std::max<int64_t>((p.S4 + kMaxChunks - 1) / kMaxChunks, g_min_chunk);
-  p.CH = (ch + kTileF4 - 1) / kTileF4 * kTileF4;
-  p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
+  p.CH = std::max<int64_t>(p.S4, kTileF4);  // chunking is chosen by the launcher
+  p.nch = 1;
 }
 
 int64_t xgpu_stage_region_bytes(int64_t n) {
@@ -380,15 +529,26 @@ int64_t xgpu_stage_region_bytes(int64_t n) {
 }
 
 int launch_xgpu(XTask& T, void* stream, std::string* err) {
-  if (T.nparts < 1 || T.nparts > kMaxXParts) {
+  if (T.nparts < 1 || T.nparts > kMaxXParts || T.nlocal < 0 || T.nlocal > kMaxXLocalGroups) {
     *err = "xgpu: bad part count";
     return RP_EINVAL;
+  }
+  for (int gi = 0; gi < T.nlocal; ++gi) {
+    const XLocalGroup& G = T.lg[gi];
+    if (G.k < 1 || G.k > kMaxFusedK) {
+      *err = "xgpu: fused local groups must have 1..4 members";
+      return RP_EINVAL;
+    }
+    for (int m = 0; m < G.k; ++m)
+      if (!G.x[m] || (reinterpret_cast<uintptr_t>(G.x[m]) & 15) || (reinterpret_cast<uintptr_t>(G.g[m]) & 15)) {
+        *err = "xgpu: local replica / gradient pointers must be non-null and 16-byte aligned";
+        return RP_EINVAL;
+      }
   }
   int mmax = 0;
   for (int pi = 0; pi < T.nparts; ++pi) {
     const XPart& p = T.part[pi];
-    if (p.m < 1 || p.m > kMaxXLocal || p.kp < 2 || p.kp > kMaxXGpus || p.me < 0 || p.me >= p.kp ||
-        p.nch < 1 || p.nch > kMaxChunks) {
+    if (p.m < 1 || p.m > kMaxXLocal || p.kp < 2 || p.kp > kMaxXGpus || p.me < 0 || p.me >= p.kp) {
       *err = "xgpu: bad part descriptor";
       return RP_EINVAL;
     }
@@ -404,11 +564,12 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   // wait on each other across GPUs), so M is the largest local member count
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (g_u < 0) {
-    g_u = env_int("RP_XGPU_U", 2);
+    g_u = env_int("RP_XGPU_U", 4);
     g_cps = env_int("RP_XGPU_CTAS_PER_SM", 0);
+    g_lag = env_int("RP_XGPU_LAG", 0);
   }
   if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4>(T, s, err) : (g_u == 1 ? launch_m<1, 1>(T, s, err) : launch_m<1, 2>(T, s, err));
-  if (mmax <= 2) return g_u >= 4 ? launch_m<2, 4>(T, s, err) : (g_u == 1 ? launch_m<2, 1>(T, s, err) : launch_m<2, 2>(T, s, err));
+  if (mmax <= 2) return g_u == 1 ? launch_m<2, 1>(T, s, err) : launch_m<2, 2>(T, s, err);  // U=4 spills
   if (mmax <= 4) return launch_m<4, 1>(T, s, err);
   return launch_m<8, 1>(T, s, err);
 }

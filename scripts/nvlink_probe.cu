@@ -52,6 +52,52 @@ __global__ void peer_write(const float4* __restrict__ src, float4* __restrict__ 
   }
 }
 
+// item_A-like: read x and g locally, y = x - 0.1 g, store y to the peer; per CH float4 chunk
+// (one CTA per chunk, chunks strided over the grid) optional fence.sys + flag
+template <int U, bool ASM, bool FENCE>
+__global__ void push_like(const float4* __restrict__ x, const float4* __restrict__ g, float4* __restrict__ dst,
+                          long n4, long ch, unsigned long long* flag) {
+  const long nch = (n4 + ch - 1) / ch;
+  for (long c = blockIdx.x; c < nch; c += gridDim.x) {
+    const long lo = c * ch, hi = min(lo + ch, n4);
+    for (long t0 = lo; t0 < hi; t0 += 256 * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long i = t0 + u * 256 + threadIdx.x;
+        if (i < hi) {
+          float4 a, b;
+          if (ASM) {
+            asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(x + i));
+            asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(g + i));
+          } else {
+            a = x[i];
+            b = g[i];
+          }
+          v[u] = make_float4(a.x - 0.1f * b.x, a.y - 0.1f * b.y, a.z - 0.1f * b.z, a.w - 0.1f * b.w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long i = t0 + u * 256 + threadIdx.x;
+        if (i < hi) {
+          if (ASM)
+            asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + i), "f"(v[u].x), "f"(v[u].y), "f"(v[u].z), "f"(v[u].w) : "memory");
+          else
+            dst[i] = v[u];
+        }
+      }
+    }
+    if (FENCE) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag + c), "l"((unsigned long long)c + 1) : "memory");
+      }
+    }
+  }
+}
+
 template <typename K>
 float time_kernel(int dev, K launch, int reps) {
   cudaSetDevice(dev);
@@ -144,6 +190,58 @@ int main() {
     cudaEventElapsedTime(&ms, s0, e0);
     printf("bidir write (each GPU writes the other) grid=%d: %7.1f GB/s per direction\n", grid,
            bytes * 10 / ms / 1e6);
+  }
+  {
+    // item_A-like pushes, both GPUs at once (GPU0 -> GPU1 and GPU1 -> GPU0), 256 MiB each
+    unsigned long long *f0, *f1;
+    cudaSetDevice(0);
+    cudaMalloc(&f0, 1 << 20);
+    cudaSetDevice(1);
+    cudaMalloc(&f1, 1 << 20);
+    const long m4 = n4 / 2;
+    auto both = [&](auto k0, auto k1, const char* name) {
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaSetDevice(0);
+        cudaDeviceSynchronize();
+        cudaSetDevice(1);
+        cudaDeviceSynchronize();
+        cudaSetDevice(0);
+        cudaEvent_t s0, e0;
+        cudaEventCreate(&s0);
+        cudaEventCreate(&e0);
+        cudaEventRecord(s0);
+        for (int r = 0; r < 5; ++r) {
+          cudaSetDevice(0);
+          k0();
+          cudaSetDevice(1);
+          k1();
+        }
+        cudaSetDevice(1);
+        cudaDeviceSynchronize();
+        cudaSetDevice(0);
+        cudaEventRecord(e0);
+        cudaEventSynchronize(e0);
+        float ms;
+        cudaEventElapsedTime(&ms, s0, e0);
+        if (rep == 1) printf("%-52s: %7.1f GB/s per direction\n", name, m4 * 16.0 * 5 / ms / 1e6);
+      }
+    };
+    const int grid = sms * 2;
+    for (long ch : {2048L, 8192L, 65536L}) {
+      char nm[128];
+      snprintf(nm, sizeof nm, "push-like C++ U4 ch=%ld nofence", ch);
+      both([&] { push_like<4, false, false><<<grid, 256>>>(a0, b0, b1, m4, ch, f0); },
+           [&] { push_like<4, false, false><<<grid, 256>>>(a1, b1, b0, m4, ch, f1); }, nm);
+      snprintf(nm, sizeof nm, "push-like asm U4 ch=%ld nofence", ch);
+      both([&] { push_like<4, true, false><<<grid, 256>>>(a0, b0, b1, m4, ch, f0); },
+           [&] { push_like<4, true, false><<<grid, 256>>>(a1, b1, b0, m4, ch, f1); }, nm);
+      snprintf(nm, sizeof nm, "push-like asm U4 ch=%ld fence+flag", ch);
+      both([&] { push_like<4, true, true><<<grid, 256>>>(a0, b0, b1, m4, ch, f0); },
+           [&] { push_like<4, true, true><<<grid, 256>>>(a1, b1, b0, m4, ch, f1); }, nm);
+      snprintf(nm, sizeof nm, "push-like C++ U4 ch=%ld fence+flag", ch);
+      both([&] { push_like<4, false, true><<<grid, 256>>>(a0, b0, b1, m4, ch, f0); },
+           [&] { push_like<4, false, true><<<grid, 256>>>(a1, b1, b0, m4, ch, f1); }, nm);
+    }
   }
   float ms = time_kernel(0, [&] { cudaMemcpyPeerAsync(b0, 0, a1, 1, bytes); }, 10);
   printf("cudaMemcpyPeerAsync 1->0: %7.1f GB/s\n", bytes / ms / 1e6);

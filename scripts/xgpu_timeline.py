@@ -1,0 +1,46 @@
+#!/usr/bin/env python3
+"""Analyse the cross-GPU kernel item timeline dumped with RP_XGPU_PROFILE=path (files path.<rank>).
+
+Each record: t_start, t_ready (wait satisfied), t_end (flag posted) in %globaltimer ns, meta.
+"""
+import sys
+
+import numpy as np
+
+KIND = {0: "A", 1: "B", 2: "C"}
+
+
+def main():
+    for path in sys.argv[1:]:
+        rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 4)
+        rec = rec[rec[:, 0] > 0]
+        t0 = rec[:, 0].min()
+        ts, tr, te = [(rec[:, i] - t0).astype(np.float64) / 1e3 for i in range(3)]  # us
+        kind = (rec[:, 3] >> np.uint64(62)).astype(int)
+        cta = ((rec[:, 3] >> np.uint64(32)) & np.uint64(0xFFFFFF)).astype(int)
+        print(f"== {path}: {len(rec)} items, kernel span {te.max():.1f} us, CTAs {cta.max() + 1}")
+        for k in (0, 1, 2):
+            m = kind == k
+            if not m.any():
+                continue
+            wait = tr[m] - ts[m]
+            work = te[m] - tr[m]
+            print(f"  {KIND[k]}: n={m.sum():5d}  first start {ts[m].min():8.1f}  last end {te[m].max():8.1f}  "
+                  f"wait mean {wait.mean():7.2f} max {wait.max():7.2f}  work mean {work.mean():7.2f} "
+                  f"p50 {np.median(work):7.2f} max {work.max():7.2f} us")
+        span = te.max()
+        bucket = max(10.0, span / 15)
+        print(f"  t(us)   work-A  work-B  work-C  waiting   (CTAs busy, averaged per {bucket:.0f} us bucket)")
+        t = 0.0
+        while t < span:
+            lo, hi = t, t + bucket
+
+            def occ(a, z):
+                return np.clip(np.minimum(z, hi) - np.maximum(a, lo), 0, None).sum() / bucket
+            line = [occ(tr[kind == k], te[kind == k]) for k in (0, 1, 2)] + [occ(ts, tr)]
+            print(f"  {lo:7.0f}  " + "  ".join(f"{v:6.1f}" for v in line))
+            t += bucket
+
+
+if __name__ == "__main__":
+    main()
