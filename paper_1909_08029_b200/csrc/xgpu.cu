@@ -404,6 +404,15 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
 
 int g_sms = 0;
 
+// Tuning knobs (read once): RP_XGPU_U (1|2|4 float4 per thread and tile row),
+// RP_XGPU_CTAS_PER_SM (cap on resident CTAs used), RP_XGPU_CHUNK_F4 (min chunk).
+int env_int(const char* name, int def) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : def;
+}
+int g_u = -1, g_cps = -1, g_lag = -1;
+int64_t g_min_chunk = -1;
+
 // Host-built work-item order, cached per launch shape. Virtual time in units of a
 // part's chunks: A(o, c) at c, B(c) at c + lag, C(o, c) at c + 2 lag; L items spread
 // evenly over the A and B items. The default lag = nch runs all A items, then all B
@@ -462,14 +471,6 @@ int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count
   return RP_OK;
 }
 
-// Tuning knobs (read once): RP_XGPU_U (1|2|4 float4 per thread and tile row),
-// RP_XGPU_CTAS_PER_SM (cap on resident CTAs used), RP_XGPU_CHUNK_F4 (min chunk).
-int env_int(const char* name, int def) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : def;
-}
-int g_u = -1, g_cps = -1, g_lag = -1;
-int64_t g_min_chunk = -1;
 
 template <int M, int U>
 int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
