@@ -42,6 +42,9 @@ WORKLOADS = {
     "cfg4": dict(desc="configs[3]: 2 workers per B200 (16 on 8 GPUs), VGG-16-sized 138M fp32, k=3, static "
                       "SHIFT_K(2N,3)",
                  wpg=2, n=N_VGG, k=3, mode="static", rule="shift_k"),
+    "cfg5": dict(desc="configs[4]: 2 workers per B200, VGG-16-sized, k=3, asynchronous GB+GD+filter (C_thres=4), "
+                      "worker 0 slowed by --slow x T_c of device delay per step (P:1395)",
+                 wpg=2, n=N_VGG, k=3, mode="async", rule=None),
 }
 NVLINK_PEAK = 770.0   # GB/s per direction, measured peer copy (B200_PROFILING.md)
 NVLINK_NOMINAL = 900.0
@@ -271,6 +274,71 @@ def run_ours(args, wl):
     print(json.dumps(out), flush=True)
 
 
+def run_async(args, wl):
+    """configs[4]: one host thread per worker, one shared GG, synthetic compute T_c per step on
+    the worker's stream (slowed worker: (1 + s) T_c, reading R13), for a fixed wall-clock window;
+    value = worker-steps completed inside the window / window, all ranks."""
+    import random
+    import torch
+    import paper_1909_08029_b200 as rp
+    from paper_1909_08029_b200.async_runner import AsyncRunner
+
+    rank, local_rank, n_gpus = init_dist(args)
+    torch.cuda.set_device(local_rank)
+    pg = setup_dist(n_gpus, local_rank)
+    wpg, n = wl["wpg"], wl["n"]
+    world = wpg * n_gpus
+    k = min(wl["k"], world)
+    job = [random.getrandbits(62) + 1]
+    if pg is not None:
+        import torch.distributed as dist
+        dist.broadcast_object_list(job, src=0, group=pg)
+    r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
+                    job_id=job[0], peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
+    tc = int(args.tc_us * 1000)
+    slow = float(args.slow)
+
+    def delay(w):
+        return int(tc * (1 + slow)) if w == 0 else tc
+    r.run(steps=max(3, args.warmup), delay_ns=delay)          # warm-up (then everybody retired)
+    r.close()
+    r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
+                    job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
+    barrier(pg)
+    with ClockSampler(local_rank) as clk:
+        done = r.run(window_s=args.window, delay_ns=delay)
+    st = r.ctx.stats()
+    tim = r.ctx.timing_read()
+    per_rank = gather({"done": done, "tim": tim, "st": st, "clocks": clk.summary()}, pg)
+    r.close()
+    if rank != 0:
+        return
+    steps = {w: v for d in per_rank for w, v in d["done"].items()}
+    total = sum(steps.values())
+    x_ms = sum(d["tim"]["cross_ms"] for d in per_rank)
+    x_b = sum(d["tim"]["cross_bytes_nvlink"] for d in per_rank)
+    out = {
+        "metric": "worker-steps/s (P-Reduce GB/s vs NVLink/HBM roofline; worker-steps/sec at 1/2/4/8 B200)",
+        "value": round(total / args.window, 1), "unit": "worker-steps/s", "n_gpus": n_gpus,
+        "steps": total, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "impl": "ours", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "world": world, "workers_per_gpu": wpg,
+                   "n_params": n, "group_size": k, "c_thres": 4, "slow_factor": slow, "tc_us": args.tc_us,
+                   "window_s": args.window,
+                   "steps_per_worker": [steps[w] for w in sorted(steps)],
+                   "gd_calls": per_rank[0]["st"]["gd_calls"],
+                   "cross_gpu_groups": sum(d["st"]["cross_gpu_groups"] for d in per_rank),
+                   "groups_launched": sum(d["st"]["groups_launched"] for d in per_rank)},
+        "roofline": ({"bound": "nvlink", "kernel": "xgpu_kernel (async cross-GPU groups)",
+                      "achieved": round(x_b / (x_ms / 1e3) / 1e9, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
+                      "frac": round(x_b / (x_ms / 1e3) / 1e9 / NVLINK_PEAK, 4)} if x_ms > 0 else None),
+        "gpu_launches": sum(d["st"]["kernel_launches"] for d in per_rank),
+        "clocks": next((d["clocks"] for d in per_rank if d["clocks"]), None),
+        "e2e": None,
+    }
+    print(json.dumps(out), flush=True)
+
+
 def run_nccl_ar(args, wl):
     """Baseline: global All-Reduce (Horovod/NCCL in the paper) of every
     worker's SGD-updated replica: local SGD + pre-sum of the GPU's workers, ncclAllReduce(sum),
@@ -291,7 +359,16 @@ def run_nccl_ar(args, wl):
     G = torch.rand((wpg, n), device="cuda") * 2 - 1
     lr = 0.1
 
+    stream = torch.cuda.current_stream()
+    delay_ns = 0
+    if wl["mode"] == "async":       # configs[4]: every step waits for the slowest worker's compute
+        import paper_1909_08029_b200 as rp
+        tc = int(args.tc_us * 1000)
+        delay_ns = int(tc * (1 + float(args.slow))) if rank == 0 else tc
+
     def step():
+        if delay_ns:
+            rp.compute_delay(stream.cuda_stream, delay_ns)
         X.sub_(G, alpha=lr)
         s = X.sum(0) if wpg > 1 else X[0].clone()
         if n_gpus > 1:
@@ -316,6 +393,7 @@ def run_nccl_ar(args, wl):
         print(json.dumps({
             "metric": "worker-steps/s (P-Reduce GB/s vs NVLink/HBM roofline; worker-steps/sec at 1/2/4/8 B200)",
             "value": round(world * args.steps / (ms / 1e3), 1), "unit": "worker-steps/s", "n_gpus": n_gpus,
+            "slow_factor": float(args.slow) if wl["mode"] == "async" else None,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "dtype": "f32", "impl": "nccl-allreduce-baseline",
             "busbw_gbs": round(bus * args.steps / (ms / 1e3) / 1e9, 1) if bus else None,
@@ -383,7 +461,7 @@ def oracle_steps(wl, n_gpus, sample, steps):
     X = {w: gen.x0(w, wl["n"], 0, sample) for w in range(world)}
     G = {w: gen.grad(w, 1, wl["n"], 0, sample) for w in range(world)}
     k = min(wl["k"], world)
-    gg = GroupGenerator(world, k, c_thres=4, seed_gd=3) if wl["mode"] == "gd" else None
+    gg = GroupGenerator(world, k, c_thres=4, seed_gd=3) if wl["mode"] in ("gd", "async") else None
     lr = np.float32(0.1)
     t0 = time.perf_counter()
     for t in range(1, steps + 1):
@@ -467,6 +545,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
+    ap.add_argument("--tc-us", type=float, default=2000.0, help="cfg5: synthetic compute time per step")
+    ap.add_argument("--window", type=float, default=3.0, help="cfg5: measured wall-clock window (s)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
@@ -477,6 +558,8 @@ def main():
         run_reference(args, wl)
     elif args.impl == "nccl":
         run_nccl_ar(args, wl)
+    elif wl["mode"] == "async":
+        run_async(args, wl)
     else:
         run_ours(args, wl)
 

@@ -66,6 +66,11 @@ extern "C" {
 #define RP_FLAG_TRACE 0x1       /* keep the JSONL decision trace (rp_trace_open)       */
 #define RP_FLAG_TIMING 0x2      /* bracket every kernel launch with CUDA timing events
                                    on its own stream (rp_timing_read)                   */
+#define RP_FLAG_SHARED_GG 0x4   /* multi-process asynchronous runs: ONE Group Generator
+                                   in POSIX shared memory "/rp_gg_<job_id>" (created by
+                                   rank 0, mapped by the others), serialized by a
+                                   process-shared mutex; cross-GPU groups may then be
+                                   issued outside batches (launched in GG order)       */
 
 #define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
 #define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */
@@ -82,7 +87,9 @@ typedef struct rp_config {
   int32_t nodes;           /* PAPER4 node count (world = nodes * m); 0 = n_gpus          */
   uint64_t seed_gd;        /* splitmix64 seed of the GD random partition (reading R8)    */
   int32_t flags;           /* RP_FLAG_*                                                  */
-  int32_t reserved[7];
+  int32_t reserved0;
+  uint64_t job_id;         /* RP_FLAG_SHARED_GG: same nonzero value on every rank        */
+  int32_t reserved[4];
 } rp_config;
 
 /* One group: members ascending. seq >= 0: granted by the GG (creation order);
@@ -278,7 +285,14 @@ const char* rp_last_error(void);
 const char* rp_strerror(int status);
 int rp_abi_version(void);
 
-/* ---- synthetic inputs (harness kernel, not part of the method) ----------------------- */
+/* ---- synthetic inputs and compute (harness kernels, not part of the method) ----------- */
+
+/* Enqueue a device-side busy wait of `ns` nanoseconds on `stream` (one thread
+ * spinning on %globaltimer): the synthetic per-step compute time T_c of the
+ * heterogeneity runs ("adding ... times the normal iteration time of sleep",
+ * P:1395; reading R13). Errors: RP_EINVAL (ns < 0), RP_ECUDA. */
+int rp_compute_delay(void* stream, int64_t ns);
+
 /* dst[i] = xi(seed, w, t, j0 + i) for i < n on `stream` (cudaStream_t as void*),
  * the counter-based generator of DESIGN.md "Input recipe" (splitmix64
  * finalizer; bit-identical to rp_inputs/gen.py). dst must be 4-byte aligned

@@ -13,6 +13,11 @@
 //    has waited the GG releases the group (Group Buffer pop, lock bits clear,
 //    P:741-742) and the trace logs "done".
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <pthread.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <condition_variable>
@@ -23,6 +28,7 @@
 #include <mutex>
 #include <algorithm>
 #include <new>
+#include <set>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -101,6 +107,17 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 }  // namespace
 
+// One Group Generator shared by all ranks of an asynchronous multi-process job
+// (RP_FLAG_SHARED_GG): POSIX shared memory, process-shared mutex ("generates
+// groups in a serial manner").
+struct SharedGG {
+  uint64_t magic;          // written last by the creator
+  pthread_mutex_t mu;
+  int64_t trace_n;         // global decision-trace event counter
+  rp::GGState gg;
+};
+constexpr uint64_t kSharedMagic = 0x52505f47475f3031ull;  // "RP_GG_01"
+
 struct rp_ctx {
   rp_config cfg{};
   bool has_gpu = false;
@@ -109,7 +126,14 @@ struct rp_ctx {
   WorkerSlot w[RP_MAX_WORLD];
   std::map<int64_t, ActiveGroup> active;
   uint64_t inflight = 0;  // engine lock vector: members of launched, un-waited groups
-  rp::GGState gg{};
+  rp::GGState gg{};           // private GG (single process, or replicated in lockstep)
+  rp::GGState* ggp = &gg;      // the GG in use (private or shared)
+  SharedGG* shm = nullptr;     // RP_FLAG_SHARED_GG
+  std::string shm_name;
+  int64_t trace_local_n = 0;
+  cudaStream_t comm = nullptr;      // asynchronous cross-GPU launches, in GG order
+  std::set<int64_t> xready;         // cross GG groups whose local members all arrived
+  std::set<int64_t> xlaunched;      // cross GG groups this GPU has launched
   rp_stats stats{};
   FILE* trace = nullptr;
   bool batching = false;
@@ -138,10 +162,24 @@ struct rp_ctx {
 
 namespace {
 
-void trace_line(rp_ctx* c, const std::string& s) {
+// Serializes Group Generator decisions across processes (no-op for a private GG,
+// which the context mutex already protects). Lock order: ctx->mu, then GGLock.
+struct GGLock {
+  pthread_mutex_t* m;
+  explicit GGLock(rp_ctx* c) : m(c->shm ? &c->shm->mu : nullptr) {
+    if (m) pthread_mutex_lock(m);
+  }
+  ~GGLock() {
+    if (m) pthread_mutex_unlock(m);
+  }
+};
+
+// Append one decision-trace event; "n" orders events of all ranks (GG order).
+// Caller holds ctx->mu and the GGLock.
+void trace_line(rp_ctx* c, const std::string& body) {
+  const int64_t n = c->shm ? c->shm->trace_n++ : c->trace_local_n++;
   if (!c->trace) return;
-  std::fputs(s.c_str(), c->trace);
-  std::fputc('\n', c->trace);
+  std::fprintf(c->trace, "{\"n\":%lld,%s}\n", static_cast<long long>(n), body.c_str());
   std::fflush(c->trace);
 }
 
@@ -177,10 +215,12 @@ bool same_group(const rp_group& a, const rp_group& b) {
 
 // GG release of a completed group + trace (caller holds mu).
 int release_gg_group(rp_ctx* c, int64_t seq) {
+  GGLock lk(c);
+  if (c->shm && !rp::gg_find(c->ggp, seq)) return RP_OK;  // another rank observed it first
   rp_group rel{};
-  const int rc = rp::gg_done(&c->gg, seq, &rel);
+  const int rc = rp::gg_done(c->ggp, seq, &rel);
   if (rc != RP_OK) return rc;
-  trace_line(c, "{\"ev\":\"done\",\"seq\":" + std::to_string(seq) + "}");
+  trace_line(c, "\"ev\":\"done\",\"seq\":" + std::to_string(seq));
   return RP_OK;
 }
 
@@ -201,6 +241,8 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // ordered after the kernel and records its own completion event.
 int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
                  cudaStream_t stream);
+int pump_cross(rp_ctx* c);
+int open_shared_gg(rp_ctx* c);
 
 int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (all_seqs.empty()) return RP_OK;
@@ -405,6 +447,115 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
   return RP_OK;
 }
 
+// Launch one asynchronous cross-GPU group on the comm stream (caller holds mu).
+int launch_cross_async(rp_ctx* c, int64_t seq) {
+  ActiveGroup& a = c->active.at(seq);
+  c->stats.lock_assertions++;
+  if (c->inflight & a.local_mask)
+    return fail(RP_ECONFLICT, "atomicity violation: members " + members_str(a.g, c->inflight) +
+                                  " hold an unfinished group");
+  for (int m = 0; m < RP_MAX_WORLD; ++m)
+    if ((a.local_mask >> m) & 1) CUDA_TRY(cudaStreamWaitEvent(c->comm, c->w[m].ev_arrive, 0));
+  const int rc = launch_cross(c, {seq}, {}, c->comm);
+  if (rc != RP_OK) return rc;
+  WorkerSlot& L = c->w[__builtin_ctzll(a.local_mask)];
+  CUDA_TRY(cudaEventRecord(L.ev_group, c->comm));
+  for (int m = 0; m < RP_MAX_WORLD; ++m) {
+    if (!((a.local_mask >> m) & 1)) continue;
+    CUDA_TRY(cudaStreamWaitEvent(c->w[m].stream, L.ev_group, 0));
+    CUDA_TRY(cudaEventRecord(c->w[m].ev_done, c->w[m].stream));
+  }
+  a.launched = true;
+  c->inflight |= a.local_mask;
+  c->cv.notify_all();
+  return RP_OK;
+}
+
+// Launch ready asynchronous cross-GPU groups in GG (seq) order: group s may go
+// only when no live cross-GPU group with a smaller seq that involves this GPU is
+// still unlaunched here. Every GPU then runs its spinning parts in one global
+// order, so no two GPUs can wait on each other's later group (the lowest live
+// group can always complete). Caller holds mu.
+int pump_cross(rp_ctx* c) {
+  const int wpg = c->cfg.workers_per_gpu;
+  while (!c->xready.empty()) {
+    const int64_t s = *c->xready.begin();
+    bool blocked = false;
+    {
+      GGLock gl(c);
+      for (const auto& g : c->ggp->table) {
+        if (g.seq < 0 || g.seq >= s || c->xlaunched.count(g.seq)) continue;
+        bool mine = false, other = false;
+        for (int i = 0; i < g.size; ++i) (g.members[i] / wpg == c->cfg.rank ? mine : other) = true;
+        if (mine && other) {
+          blocked = true;
+          break;
+        }
+      }
+    }
+    if (blocked) return RP_OK;
+    c->xready.erase(s);
+    c->xlaunched.insert(s);
+    const int rc = launch_cross_async(c, s);
+    if (rc != RP_OK) return rc;
+  }
+  return RP_OK;
+}
+
+int open_shared_gg(rp_ctx* c) {
+  const rp_config& k = c->cfg;
+  // n_gpus == 0 (host-only) is allowed so the multi-process GG can be tested without GPUs
+  if (k.n_gpus == 1 || k.job_id == 0) return fail(RP_EINVAL, "RP_FLAG_SHARED_GG needs n_gpus != 1 and a job_id");
+  c->shm_name = "/rp_gg_" + std::to_string(static_cast<unsigned long long>(k.job_id));
+  const size_t size = sizeof(SharedGG);
+  int fd = -1;
+  if (k.rank == 0) {
+    shm_unlink(c->shm_name.c_str());
+    fd = shm_open(c->shm_name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0 || ftruncate(fd, static_cast<off_t>(size)) != 0) {
+      if (fd >= 0) close(fd);
+      return fail(RP_ENOMEM, "shared GG: cannot create " + c->shm_name);
+    }
+  } else {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      fd = shm_open(c->shm_name.c_str(), O_RDWR, 0600);
+      struct stat st {};
+      if (fd >= 0 && fstat(fd, &st) == 0 && static_cast<size_t>(st.st_size) >= size) break;
+      if (fd >= 0) close(fd);
+      fd = -1;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        return fail(RP_ETIMEOUT, "shared GG: " + c->shm_name + " not created by rank 0");
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+  }
+  void* p = mmap(nullptr, size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return fail(RP_ENOMEM, "shared GG: mmap failed");
+  c->shm = static_cast<SharedGG*>(p);
+  if (k.rank == 0) {
+    pthread_mutexattr_t at;
+    pthread_mutexattr_init(&at);
+    pthread_mutexattr_setpshared(&at, PTHREAD_PROCESS_SHARED);
+    pthread_mutex_init(&c->shm->mu, &at);
+    pthread_mutexattr_destroy(&at);
+    c->shm->trace_n = 0;
+    rp::gg_init(&c->shm->gg, k.world, k.group_size, k.c_thres, k.seed_gd);
+    __atomic_store_n(&c->shm->magic, kSharedMagic, __ATOMIC_RELEASE);
+  } else {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (__atomic_load_n(&c->shm->magic, __ATOMIC_ACQUIRE) != kSharedMagic) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        return fail(RP_ETIMEOUT, "shared GG: rank 0 never initialized " + c->shm_name);
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  }
+  c->ggp = &c->shm->gg;
+  if (c->ggp->n != k.world || c->ggp->k != k.group_size)
+    return fail(RP_EINVAL, "shared GG: configuration differs between ranks");
+  return RP_OK;
+}
+
 using CuMemGetAddressRange = int (*)(uintptr_t*, size_t*, uintptr_t);
 
 // Allocation base of a device pointer (driver entry point; no link-time libcuda).
@@ -464,6 +615,13 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
   c->cfg = k;
   if (c->cfg.workers_per_gpu < 1) c->cfg.workers_per_gpu = k.world;
   rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd);
+  if (k.flags & RP_FLAG_SHARED_GG) {
+    const int rc = open_shared_gg(c);
+    if (rc != RP_OK) {
+      rp_finalize(c);
+      return rc;
+    }
+  }
   if (k.n_gpus > 0) {
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -495,6 +653,10 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       s.own_stream = true;
     }
     if (k.n_gpus > 1) {
+      if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess) {
+        rp_finalize(c);
+        return cuda_fail(e, "rp_init: comm stream");
+      }
       if (const char* pp = std::getenv("RP_XGPU_PROFILE")) c->prof_path = pp;
       if (wpg > RP_MAX_LOCAL) {
         rp_finalize(c);
@@ -607,6 +769,10 @@ int rp_finalize(rp_ctx* c) {
       cudaEventDestroy(t.stop);
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    if (c->comm) {
+      cudaStreamSynchronize(c->comm);
+      cudaStreamDestroy(c->comm);
+    }
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (c->flags) cudaFree(c->flags);
     if (c->stage) cudaFree(c->stage);
@@ -631,6 +797,10 @@ int rp_finalize(rp_ctx* c) {
     }
   }
   if (c->trace) std::fclose(c->trace);
+  if (c->shm) {
+    munmap(c->shm, sizeof(SharedGG));
+    if (c->cfg.rank == 0) shm_unlink(c->shm_name.c_str());
+  }
   delete c;
   return RP_OK;
 }
@@ -716,21 +886,23 @@ int rp_schedule_static_worker(rp_ctx* c, int32_t rule, int64_t step, int32_t w, 
 int rp_group_generate(rp_ctx* c, int32_t w, rp_group* out) {
   if (!c || !out) return fail(RP_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
-  const int rc = rp::gg_request(&c->gg, w, out);
+  GGLock gl(c);
+  const int rc = rp::gg_request(c->ggp, w, out);
   if (rc != RP_OK) return rc;
   c->stats.gg_requests++;
-  trace_line(c, "{\"ev\":\"req\",\"w\":" + std::to_string(w) + "," + group_json(*out) + "}");
+  trace_line(c, "\"ev\":\"req\",\"w\":" + std::to_string(w) + "," + group_json(*out));
   return RP_OK;
 }
 
 int rp_group_generate_many(rp_ctx* c, const int32_t* workers, int32_t n, rp_group* out) {
   if (!c || (n > 0 && (!workers || !out)) || n < 0) return fail(RP_EINVAL, "bad argument");
   std::lock_guard<std::mutex> lk(c->mu);
+  GGLock gl(c);
   for (int i = 0; i < n; ++i) {
-    const int rc = rp::gg_request(&c->gg, workers[i], &out[i]);
+    const int rc = rp::gg_request(c->ggp, workers[i], &out[i]);
     if (rc != RP_OK) return rc;
     c->stats.gg_requests++;
-    trace_line(c, "{\"ev\":\"req\",\"w\":" + std::to_string(workers[i]) + "," + group_json(out[i]) + "}");
+    trace_line(c, "\"ev\":\"req\",\"w\":" + std::to_string(workers[i]) + "," + group_json(out[i]));
   }
   return RP_OK;
 }
@@ -745,8 +917,9 @@ int rp_gg_release(rp_ctx* c, int64_t seq) {
 int rp_retire(rp_ctx* c, int32_t w) {
   if (!c) return fail(RP_EINVAL, "null ctx");
   std::lock_guard<std::mutex> lk(c->mu);
-  const int rc = rp::gg_retire(&c->gg, w);
-  if (rc == RP_OK) trace_line(c, "{\"ev\":\"retire\",\"w\":" + std::to_string(w) + "}");
+  GGLock gl(c);
+  const int rc = rp::gg_retire(c->ggp, w);
+  if (rc == RP_OK) trace_line(c, "\"ev\":\"retire\",\"w\":" + std::to_string(w));
   return rc;
 }
 
@@ -783,8 +956,9 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
     return fail(RP_ESTATE, "rp_preduce: worker " + std::to_string(w) + " has not waited for group " +
                                std::to_string(s.seq));
   if (g->seq >= 0) {  // GG group: must be the one handed to w
-    const rp::GGGroup* gg = rp::gg_find(&c->gg, g->seq);
-    bool ok = gg && c->gg.handed[w] == g->seq && gg->size == g->size;
+    GGLock gl(c);
+    const rp::GGGroup* gg = rp::gg_find(c->ggp, g->seq);
+    bool ok = gg && c->ggp->handed[w] == g->seq && gg->size == g->size;
     for (int i = 0; ok && i < g->size; ++i) ok = gg->members[i] == g->members[i];
     if (!ok) return fail(RP_EPROTO, "rp_preduce: group " + std::to_string(g->seq) + " was not handed to worker " +
                                         std::to_string(w) + " by the GG");
@@ -804,9 +978,10 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
   }
   ActiveGroup& a = it->second;
   if ((a.arrived >> w) & 1) return fail(RP_EPROTO, "rp_preduce: worker arrived twice");
-  if (a.local_mask != a.members_mask && !c->batching)
+  if (a.local_mask != a.members_mask && !c->batching && !(c->shm && g->seq >= 0))
     return fail(RP_ESTATE, "rp_preduce: a cross-GPU group must be issued inside rp_batch_begin/end "
-                           "(one launch per GPU and step keeps the GPUs' launch orders consistent)");
+                           "(one launch per GPU and step keeps the GPUs' launch orders consistent), "
+                           "or be a shared-GG group (RP_FLAG_SHARED_GG)");
   int idx = 0;
   while (g->members[idx] != w) ++idx;
   a.grad[idx] = s.staged ? s.grad : nullptr;
@@ -820,6 +995,10 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
     if (c->batching) {
       c->ready.push_back(g->seq);
       return RP_OK;
+    }
+    if (a.local_mask != a.members_mask) {  // asynchronous cross-GPU group: GG order
+      c->xready.insert(g->seq);
+      return pump_cross(c);
     }
     return launch_groups(c, {g->seq});
   }
@@ -873,7 +1052,10 @@ int rp_barrier_free_wait(rp_ctx* c, int32_t w, int64_t timeout_us) {
     a.released = true;
     if (seq >= 0) rc = release_gg_group(c, seq);
   }
-  if ((a.waited & a.local_mask) == a.local_mask) c->active.erase(seq);
+  if ((a.waited & a.local_mask) == a.local_mask) {
+    c->active.erase(seq);
+    c->xlaunched.erase(seq);
+  }
   return rc;
 }
 
@@ -936,8 +1118,9 @@ int rp_stats_get(rp_ctx* c, rp_stats* out) {
   if (!c || !out) return fail(RP_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   *out = c->stats;
-  out->gd_calls = c->gg.gd_calls;
-  out->max_gb_depth = c->gg.max_depth;
+  GGLock gl(c);
+  out->gd_calls = c->ggp->gd_calls;
+  out->max_gb_depth = c->ggp->max_depth;
   return RP_OK;
 }
 
@@ -948,6 +1131,12 @@ int rp_trace_open(rp_ctx* c, const char* path) {
   c->trace = std::fopen(path, "w");
   if (!c->trace) return fail(RP_EINVAL, std::string("cannot open trace file ") + path);
   return RP_OK;
+}
+
+int rp_compute_delay(void* stream, int64_t ns) {
+  std::string err;
+  const int rc = rp::launch_delay(stream, ns, &err);
+  return rc == RP_OK ? rc : fail(rc, err);
 }
 
 int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0, void* stream) {

@@ -138,6 +138,7 @@ void xgpu_geometry(XPart& p, int64_t n);
 int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
+int launch_delay(void* stream, int64_t ns, std::string* err);
 int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                    void* stream, std::string* err);
 

@@ -1,4 +1,4 @@
-// Synthetic input generator (harness kernel; not part of the method).
+// Synthetic input generator and compute delay (harness kernels; not part of the method).
 //
 // xi(s, w, t, j) = float32(MIX(KEY) >> 40) * 2^-23 - 1, with
 // KEY = s*0x9E3779B97F4A7C15 + w*0xD1B54A32D192ED03 + t*0x8CB92BA72F3D8DD7 + j (mod 2^64)
@@ -69,6 +69,30 @@ int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t,
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("rp_fill_xi: ") + cudaGetErrorString(e);
+    return RP_ECUDA;
+  }
+  return RP_OK;
+}
+
+__global__ void delay_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+int launch_delay(void* stream, int64_t ns, std::string* err) {
+  if (ns < 0) {
+    *err = "rp_compute_delay: negative duration";
+    return RP_EINVAL;
+  }
+  if (ns == 0) return RP_OK;
+  delay_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<unsigned long long>(ns));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("rp_compute_delay: ") + cudaGetErrorString(e);
     return RP_ECUDA;
   }
   return RP_OK;

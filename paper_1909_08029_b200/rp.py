@@ -24,6 +24,7 @@ RP_MAX_WORLD = 64
 RP_MAX_GROUP = 16
 RP_FLAG_TRACE = 0x1
 RP_FLAG_TIMING = 0x2
+RP_FLAG_SHARED_GG = 0x4
 RP_SCHED_PAPER4 = 1
 RP_SCHED_SHIFT_K = 2
 RP_WAIT_DEVICE = -1
@@ -48,7 +49,9 @@ class rp_config(ctypes.Structure):
         ("nodes", ctypes.c_int32),
         ("seed_gd", ctypes.c_uint64),
         ("flags", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("reserved0", ctypes.c_int32),
+        ("job_id", ctypes.c_uint64),
+        ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -152,6 +155,7 @@ _SIGNATURES = {
     "rp_last_error": (ctypes.c_char_p, []),
     "rp_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "rp_abi_version": (ctypes.c_int, []),
+    "rp_compute_delay": (ctypes.c_int, [_P, ctypes.c_int64]),
     "rp_fill_xi": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_uint64, _P]),
 }
@@ -316,11 +320,18 @@ def rp_fill_xi(dst, n, seed, w, t, j0=0, stream=0):
 fill_xi = rp_fill_xi
 
 
+def rp_compute_delay(stream, ns):
+    _check(load_library().rp_compute_delay(_ptr(stream), int(ns)), "rp_compute_delay")
+
+
+compute_delay = rp_compute_delay
+
+
 class Context:
     """Owns one rp_ctx. Methods map 1:1 onto the C calls."""
 
     def __init__(self, world, n_params, *, n_gpus=1, workers_per_gpu=None, rank=0, device=None,
-                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0):
+                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0, job_id=0):
         cfg = rp_config()
         cfg.world = world
         cfg.n_gpus = n_gpus
@@ -333,6 +344,7 @@ class Context:
         cfg.nodes = nodes
         cfg.seed_gd = seed_gd
         cfg.flags = flags
+        cfg.job_id = job_id
         self.cfg = cfg
         self.world = world
         self.n_params = n_params

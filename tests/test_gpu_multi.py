@@ -28,10 +28,10 @@ def _free_port():
     return p
 
 
-def _run(nproc, spec, timeout=600):
+def _run(nproc, spec, timeout=600, script="multi_gpu_worker.py"):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tests", "multi_gpu_worker.py"), json.dumps(spec)]
+           os.path.join(ROOT, "tests", script), json.dumps(spec)]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert p.stdout.count("OK") == nproc, p.stdout
@@ -49,6 +49,9 @@ CASES = [
     (4, 1, 200_003, 3, "gd", None, 10, 0),                    # cfg 3 shape at 4 GPUs
     (4, 2, 200_003, 3, "static", "shift_k", 10, 0),           # cfg 4 shape at 4 GPUs
     (4, 4, 60_001, 4, "static", "paper4", 8, 0),              # PAPER4 4 nodes x 4 (fig:schedule)
+    (8, 1, 200_003, 3, "gd", None, 10, 0),                    # cfg 3 shape at 8 GPUs
+    (8, 2, 100_003, 3, "static", "shift_k", 10, 0),           # cfg 4 shape at 8 GPUs
+    (8, 8, 20_011, 3, "gd", None, 6, 0),                      # 64 workers: 8 cross parts per GPU
 ]
 
 
@@ -57,3 +60,19 @@ def test_multi_gpu_parity(gpus, wpg, n, k, mode, rule, steps, sample):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, dict(wpg=wpg, n=n, k=k, mode=mode, rule=rule, steps=steps, sample=sample))
+
+
+ASYNC_CASES = [
+    # (gpus, wpg, n, k, c_thres, steps)
+    (2, 2, 50_003, 3, 2, 10),        # cfg 5 shape at 2 GPUs: shared GG, slowed worker 0
+    (2, 1, 40_000, 2, 0, 12),        # AD-PSGD-like pairs, filter off
+    (4, 2, 30_011, 3, 4, 8),         # cfg 5 shape at 4 GPUs
+]
+
+
+@pytest.mark.parametrize("gpus,wpg,n,k,c_thres,steps", ASYNC_CASES)
+def test_multi_gpu_async_shared_gg_replay(gpus, wpg, n, k, c_thres, steps, tmp_path):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, dict(wpg=wpg, n=n, k=k, c_thres=c_thres, steps=steps, tmp=str(tmp_path)),
+         script="multi_gpu_async_worker.py")
