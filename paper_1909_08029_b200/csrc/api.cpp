@@ -471,35 +471,39 @@ int launch_cross_async(rp_ctx* c, int64_t seq) {
   return RP_OK;
 }
 
-// Launch ready asynchronous cross-GPU groups in GG (seq) order: group s may go
-// only when no live cross-GPU group with a smaller seq that involves this GPU is
-// still unlaunched here. Every GPU then runs its spinning parts in one global
-// order, so no two GPUs can wait on each other's later group (the lowest live
-// group can always complete). Caller holds mu.
+// Launch asynchronous cross-GPU groups (shared GG). A group's parts are launched
+// only once ALL its members, on every GPU, have arrived (no kernel ever spins on
+// an absent member), and every GPU launches its parts in the order in which the
+// groups became complete (the shared ticket). Two GPUs therefore never hold
+// each other's later group behind an earlier one (the lowest ticket in flight
+// can always finish), and a group waiting for a slow member delays nobody else.
+// Caller holds mu. Waiting threads call it repeatedly (remote arrivals).
 int pump_cross(rp_ctx* c) {
   const int wpg = c->cfg.workers_per_gpu;
-  while (!c->xready.empty()) {
-    const int64_t s = *c->xready.begin();
-    bool blocked = false;
+  for (;;) {
+    int64_t best = -1, best_ticket = -1;
     {
       GGLock gl(c);
+      // lowest complete (ticketed) cross group involving this GPU not launched here yet
       for (const auto& g : c->ggp->table) {
-        if (g.seq < 0 || g.seq >= s || c->xlaunched.count(g.seq)) continue;
+        if (g.seq < 0 || g.ticket < 0 || c->xlaunched.count(g.seq)) continue;
         bool mine = false, other = false;
         for (int i = 0; i < g.size; ++i) (g.members[i] / wpg == c->cfg.rank ? mine : other) = true;
-        if (mine && other) {
-          blocked = true;
-          break;
+        if (!(mine && other)) continue;
+        if (best_ticket < 0 || g.ticket < best_ticket) {
+          best_ticket = g.ticket;
+          best = g.seq;
         }
       }
     }
-    if (blocked) return RP_OK;
-    c->xready.erase(s);
-    c->xlaunched.insert(s);
-    const int rc = launch_cross_async(c, s);
+    // it must be launched before anything later; it is ours to launch once our local
+    // members' arrival is recorded here (it always is: complete => every member arrived)
+    if (best < 0 || !c->xready.count(best)) return RP_OK;
+    c->xready.erase(best);
+    c->xlaunched.insert(best);
+    const int rc = launch_cross_async(c, best);
     if (rc != RP_OK) return rc;
   }
-  return RP_OK;
 }
 
 int open_shared_gg(rp_ctx* c) {
@@ -957,9 +961,13 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
                                std::to_string(s.seq));
   if (g->seq >= 0) {  // GG group: must be the one handed to w
     GGLock gl(c);
-    const rp::GGGroup* gg = rp::gg_find(c->ggp, g->seq);
+    rp::GGGroup* gg = const_cast<rp::GGGroup*>(rp::gg_find(c->ggp, g->seq));
     bool ok = gg && c->ggp->handed[w] == g->seq && gg->size == g->size;
     for (int i = 0; ok && i < g->size; ++i) ok = gg->members[i] == g->members[i];
+    if (ok && c->shm) {  // global arrival record; the completing arrival takes the next ticket
+      gg->arrived |= 1ull << w;
+      if (gg->ticket < 0 && gg->arrived == mask) gg->ticket = c->ggp->next_ticket++;
+    }
     if (!ok) return fail(RP_EPROTO, "rp_preduce: group " + std::to_string(g->seq) + " was not handed to worker " +
                                         std::to_string(w) + " by the GG");
   }
@@ -1021,9 +1029,17 @@ int rp_barrier_free_wait(rp_ctx* c, int32_t w, int64_t timeout_us) {
     if (!a.launched) {
       if (timeout_us < 0)
         return fail(RP_ESTATE, "group " + std::to_string(seq) + " not launched; missing members " + missing(a));
-      if (!c->cv.wait_until(lk, deadline, [&] { return c->active.at(seq).launched; }))
-        return fail(RP_ETIMEOUT, "group " + std::to_string(seq) + " " + members_str(a.g) +
-                                     ": members never arrived: " + missing(c->active.at(seq)));
+      for (;;) {
+        if (c->shm) {  // remote members arrive in other processes: drive the launcher here
+          const int prc = pump_cross(c);
+          if (prc != RP_OK) return prc;
+        }
+        if (c->active.at(seq).launched) break;
+        if (std::chrono::steady_clock::now() >= deadline)
+          return fail(RP_ETIMEOUT, "group " + std::to_string(seq) + " " + members_str(a.g) +
+                                       ": members never arrived: " + missing(c->active.at(seq)));
+        c->cv.wait_for(lk, std::chrono::microseconds(c->shm ? 20 : 1000));
+      }
     }
   }
   if (timeout_us >= 0) {

@@ -88,6 +88,8 @@ static int global_division(GGState* s, int i) {
     s->lock |= bits;
     slot->seq = s->next_seq++;
     slot->size = sz;
+    slot->arrived = 0;
+    slot->ticket = -1;
     for (int t = 0; t < sz; ++t) {
       const int m = members[t];
       slot->members[t] = m;

@@ -22,9 +22,11 @@ constexpr int kGbCap = 4;        // Group Buffer depth bound (GD alone keeps dep
 constexpr int kTableCap = 256;   // live groups
 
 struct GGGroup {
-  int64_t seq;     // -1 = free slot
+  int64_t seq;       // -1 = free slot
   int32_t size;
   int32_t members[RP_MAX_GROUP];
+  uint64_t arrived;  // members that called rp_preduce (shared GG, any process)
+  int64_t ticket;    // order of complete arrival (shared GG), -1 until all members arrived
 };
 
 // Plain-old-data so it can live in process-shared memory.
@@ -40,6 +42,7 @@ struct GGState {
   uint64_t retired, retiring;     // reading R19
   GGGroup table[kTableCap];
   int64_t gd_calls, requests, max_depth;
+  int64_t next_ticket;            // complete-arrival order of groups (shared GG)
 };
 
 void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed);
