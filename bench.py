@@ -300,13 +300,13 @@ def run_async(args, wl):
 
     def delay(w):
         return int(tc * (1 + slow)) if w == 0 else tc
-    r.run(steps=max(3, args.warmup), delay_ns=delay)          # warm-up (then everybody retired)
+    r.run(steps=max(3, args.warmup), delay_ns=delay, delay_mode=args.delay)   # warm-up, then all retired
     r.close()
     r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
                     job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
     barrier(pg)
     with ClockSampler(local_rank) as clk:
-        done = r.run(window_s=args.window, delay_ns=delay)
+        done = r.run(window_s=args.window, delay_ns=delay, delay_mode=args.delay)
     st = r.ctx.stats()
     tim = r.ctx.timing_read()
     per_rank = gather({"done": done, "tim": tim, "st": st, "clocks": clk.summary()}, pg)
@@ -324,6 +324,7 @@ def run_async(args, wl):
         "vs_baseline": None, "dtype": "f32", "impl": "ours", "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"], "world": world, "workers_per_gpu": wpg,
                    "n_params": n, "group_size": k, "c_thres": 4, "slow_factor": slow, "tc_us": args.tc_us,
+                   "compute": f"{args.delay} delay per step (T_c; worker 0: (1 + slow) T_c)",
                    "window_s": args.window,
                    "steps_per_worker": [steps[w] for w in sorted(steps)],
                    "gd_calls": per_rank[0]["st"]["gd_calls"],
@@ -368,7 +369,12 @@ def run_nccl_ar(args, wl):
 
     def step():
         if delay_ns:
-            rp.compute_delay(stream.cuda_stream, delay_ns)
+            if args.delay == "host":
+                # synchronous training: compute of step t+1 starts from the averaged step-t model
+                torch.cuda.current_stream().synchronize()
+                time.sleep(delay_ns / 1e9)
+            else:
+                rp.compute_delay(stream.cuda_stream, delay_ns)
         X.sub_(G, alpha=lr)
         s = X.sum(0) if wpg > 1 else X[0].clone()
         if n_gpus > 1:
@@ -548,6 +554,8 @@ def main():
     ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
     ap.add_argument("--tc-us", type=float, default=2000.0, help="cfg5: synthetic compute time per step")
     ap.add_argument("--window", type=float, default=3.0, help="cfg5: measured wall-clock window (s)")
+    ap.add_argument("--delay", choices=["host", "device"], default="host",
+                    help="cfg5: synthetic compute as a host sleep (P:1395) or a device busy wait")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

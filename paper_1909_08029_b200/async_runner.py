@@ -3,8 +3,9 @@
 Each worker thread runs alg1 at its own pace, with no
 global barrier (P:485-487):
 
-  compute   rp_compute_delay(T_c) on the worker's stream (synthetic compute;
-            a slowed worker adds s * T_c, reading R13 / P:1395)
+  compute   synthetic compute time T_c: a host sleep ("adding ... times the normal
+            iteration time of sleep"; reading R13; a slowed worker adds
+            s * T_c), or rp_compute_delay on the worker's stream (device busy wait)
   Step 2    rp_step(w, g, lr)
   Step 3    rp_group_generate(w): Group Buffer head or a Global Division over the
             idle workers that pass the slowdown filter
@@ -68,9 +69,11 @@ class AsyncRunner:
     def g(self, w):
         return self.G[self.local.index(w), :self.n]
 
-    def run(self, *, steps=None, window_s=None, delay_ns=None, wait_timeout_us=600_000_000):
+    def run(self, *, steps=None, window_s=None, delay_ns=None, delay_mode="device", wait_timeout_us=600_000_000):
         """Run every local worker until it did `steps` steps, or until `window_s` seconds have
-        passed (then one final step each). Returns {w: steps completed} (within the window)."""
+        passed (then one final step each). Returns {w: steps completed} (within the window).
+        delay_mode: "host" sleeps delay_ns(w) on the worker's thread before each step, "device"
+        enqueues an rp_compute_delay busy wait on the worker's stream."""
         if (steps is None) == (window_s is None):
             raise ValueError("give exactly one of steps / window_s")
         done = {w: 0 for w in self.local}
@@ -86,7 +89,10 @@ class AsyncRunner:
                     t += 1
                     final = (t == steps) if steps is not None else time.perf_counter() >= t_end
                     if delay_ns is not None:
-                        rp.compute_delay(s, delay_ns(w))
+                        if delay_mode == "host":
+                            time.sleep(delay_ns(w) / 1e9)
+                        else:
+                            rp.compute_delay(s, delay_ns(w))
                     if self.grad_mode == "per_step":
                         rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, s)
                     self.ctx.step(w, None, self.lr)
