@@ -15,7 +15,9 @@
 //
 // Memory: per element and member 4 B of x and 4 B of g read, 4 B of x
 // written: 12*k bytes per element, the algorithmic minimum (DESIGN.md
-// "Roofline"). 128-bit loads/stores; each thread keeps U*2k of them in
+// "Roofline"). 128-bit loads/stores with the streaming (.cs, evict-first)
+// cache policy: nothing is reused within a step, and the working set of a
+// step (2.45 GB at configs[1]) is 20x the L2. Each thread keeps U*2k loads in
 // flight; grid = resident CTAs (148 SMs x occupancy).
 #include <cuda_runtime.h>
 
@@ -32,7 +34,7 @@ constexpr int kThreads = 256;
 
 __device__ __forceinline__ float4 ld_x(const float* p) {
   float4 v;
-  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
   return v;
@@ -40,14 +42,14 @@ __device__ __forceinline__ float4 ld_x(const float* p) {
 
 __device__ __forceinline__ float4 ld_g(const float* p) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
   return v;
 }
 
 __device__ __forceinline__ void st_x(float* p, float4 v) {
-  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
 

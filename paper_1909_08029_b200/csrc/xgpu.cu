@@ -410,7 +410,7 @@ int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : def;
 }
-int g_u = -1, g_cps = -1, g_lag = -1;
+int g_u = -1, g_cps = -1, g_lag = -1, g_order = -1;
 int64_t g_min_chunk = -1;
 
 // Host-built work-item order, cached per launch shape. Virtual time in units of a
@@ -421,7 +421,7 @@ int64_t g_min_chunk = -1;
 int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count, std::string* err) {
   static std::mutex mu;
   static std::map<std::string, std::pair<uint32_t*, int64_t>> cache;
-  std::string key = std::to_string(T.my_gpu) + "/" + std::to_string(ctas) + "/" + std::to_string(T.nlocal) + "/" +
+  std::string key = std::to_string(g_order) + "/" + std::to_string(T.my_gpu) + "/" + std::to_string(ctas) + "/" + std::to_string(T.nlocal) + "/" +
                     std::to_string(T.nchl);
   for (int pi = 0; pi < T.nparts; ++pi)
     key += "/" + std::to_string(T.part[pi].kp) + "," + std::to_string(T.part[pi].me) + "," +
@@ -459,6 +459,22 @@ int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count
   std::stable_sort(v.begin(), v.end(), [](const Ent& a, const Ent& b) { return a.t < b.t || (a.t == b.t && a.order < b.order); });
   std::vector<uint32_t> h(v.size());
   for (size_t i = 0; i < v.size(); ++i) h[i] = v[i].code;
+  if (g_order == 1) {
+    // role split: even grid slots take A/L items, odd slots B items (both in chunk order), so
+    // B(c) starts as soon as the peers' A(c) lands; C items last
+    std::vector<uint32_t> ab, bb, cc;
+    for (uint32_t x : h) ((x >> 30) == 1 ? bb : ((x >> 30) == 2 ? cc : ab)).push_back(x);
+    h.clear();
+    size_t ia = 0, ib = 0;
+    while (ia < ab.size() || ib < bb.size()) {
+      const bool slot_b = (h.size() % 2) == 1;
+      if ((slot_b && ib < bb.size()) || ia >= ab.size())
+        h.push_back(bb[ib++]);
+      else
+        h.push_back(ab[ia++]);
+    }
+    h.insert(h.end(), cc.begin(), cc.end());
+  }
   uint32_t* d = nullptr;
   if (cudaMalloc(&d, h.size() * sizeof(uint32_t)) != cudaSuccess ||
       cudaMemcpy(d, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -568,6 +584,7 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
     g_u = env_int("RP_XGPU_U", 4);
     g_cps = env_int("RP_XGPU_CTAS_PER_SM", 0);
     g_lag = env_int("RP_XGPU_LAG", 0);
+    g_order = env_int("RP_XGPU_ORDER", 0);
   }
   if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4>(T, s, err) : (g_u == 1 ? launch_m<1, 1>(T, s, err) : launch_m<1, 2>(T, s, err));
   if (mmax <= 2) return g_u == 1 ? launch_m<2, 1>(T, s, err) : launch_m<2, 2>(T, s, err);  // U=4 spills

@@ -25,9 +25,9 @@ struct Ptrs {
 template <int MODE>
 __device__ __forceinline__ float4 ldx(const float* p) {
   float4 v;
-  if (MODE == 0)
+  if (MODE == 0 || MODE == 4)
     asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  else if (MODE == 1)
+  else if (MODE == 1 || MODE == 3)
     asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   else
     asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
@@ -36,9 +36,9 @@ __device__ __forceinline__ float4 ldx(const float* p) {
 template <int MODE>
 __device__ __forceinline__ float4 ldg(const float* p) {
   float4 v;
-  if (MODE == 0)
+  if (MODE == 0 || MODE == 4)
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  else if (MODE == 1)
+  else if (MODE == 1 || MODE == 3)
     asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   else
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
@@ -46,7 +46,7 @@ __device__ __forceinline__ float4 ldg(const float* p) {
 }
 template <int MODE>
 __device__ __forceinline__ void stx(float* p, float4 v) {
-  if (MODE == 1)
+  if (MODE == 1 || MODE == 4)
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
   else
     asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
@@ -91,6 +91,14 @@ __global__ void __launch_bounds__(256, MINB) fused(Ptrs P, long n4) {
         for (int m = 0; m < K; ++m) stx<MODE>(P.x[m] + 4 * i, r);
       }
     }
+  }
+}
+
+__global__ void fill(float* p, long n, unsigned long long seed) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed * 0x9E3779B97F4A7C15ull + i;
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27; z *= 0x94D049BB133111EBull; z ^= z >> 31;
+    p[i] = (float)(z >> 40) * 0x1p-23f - 1.0f;
   }
 }
 
@@ -148,6 +156,11 @@ int main() {
   }
   float* out;
   CK(cudaMalloc(&out, 4));
+  for (int m = 0; m < K; ++m) {  // non-zero, incompressible data
+    fill<<<1184, 256>>>(P.x[m], n, 2 * m + 1);
+    fill<<<1184, 256>>>(const_cast<float*>(P.g[m]), n, 2 * m + 2);
+  }
+  CK(cudaDeviceSynchronize());
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double algo = 12.0 * K * n;
@@ -165,6 +178,9 @@ int main() {
   RUN("U4 mode0", 4, 0, 1, 1);
   RUN("U2 mode1 (.cs loads+stores)", 2, 1, 1, 2);
   RUN("U2 mode2 (L2::256B prefetch)", 2, 2, 1, 2);
+  RUN("U2 mode3 (.cs loads only)", 2, 3, 1, 2);
+  RUN("U2 mode4 (.cs stores only)", 2, 4, 1, 2);
+  RUN("U1 mode1 (.cs) grid x4", 1, 1, 1, 4);
   RUN("U1 mode2 minB4", 1, 2, 4, 4);
   RUN("U2 mode0 grid x8", 2, 0, 1, 8);
   {
