@@ -293,8 +293,10 @@ def run_async(args, wl):
     if pg is not None:
         import torch.distributed as dist
         dist.broadcast_object_list(job, src=0, group=pg)
+    if args.k:
+        k = min(args.k, world)
     r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
-                    job_id=job[0], peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
+                    job_id=job[0], peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg)
     tc = int(args.tc_us * 1000)
     slow = float(args.slow)
 
@@ -303,7 +305,7 @@ def run_async(args, wl):
     r.run(steps=max(3, args.warmup), delay_ns=delay, delay_mode=args.delay)   # warm-up, then all retired
     r.close()
     r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
-                    job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING)
+                    job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg)
     barrier(pg)
     with ClockSampler(local_rank) as clk:
         done = r.run(window_s=args.window, delay_ns=delay, delay_mode=args.delay)
@@ -324,6 +326,11 @@ def run_async(args, wl):
         "vs_baseline": None, "dtype": "f32", "impl": "ours", "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"], "world": world, "workers_per_gpu": wpg,
                    "n_params": n, "group_size": k, "c_thres": 4, "slow_factor": slow, "tc_us": args.tc_us,
+                   "group_generation": ("random GG + lock vector + pending queue (P:680-745)" +
+                                        (" = AD-PSGD" if k == 2 else "")) if args.gg == "random"
+                                       else "GB + GD + slowdown filter (P:997-1195)",
+                   "gg_pending": sum(d["st"]["gg_pending"] for d in per_rank),
+                   "gg_granted": sum(d["st"]["gg_granted"] for d in per_rank),
                    "compute": f"{args.delay} delay per step (T_c; worker 0: (1 + slow) T_c)",
                    "window_s": args.window,
                    "steps_per_worker": [steps[w] for w in sorted(steps)],
@@ -554,6 +561,9 @@ def main():
     ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
     ap.add_argument("--tc-us", type=float, default=2000.0, help="cfg5: synthetic compute time per step")
     ap.add_argument("--window", type=float, default=3.0, help="cfg5: measured wall-clock window (s)")
+    ap.add_argument("--gg", choices=["gd", "random"], default="gd",
+                    help="cfg5 group generation: GB+GD+filter (§5) or the random GG of §4.1")
+    ap.add_argument("--k", type=int, default=0, help="cfg5: group size override (2 + --gg random = AD-PSGD)")
     ap.add_argument("--delay", choices=["host", "device"], default="host",
                     help="cfg5: synthetic compute as a host sleep (P:1395) or a device busy wait")
     args = ap.parse_args()

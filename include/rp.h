@@ -61,6 +61,8 @@ extern "C" {
 #define RP_ECUDA (-6)     /* CUDA runtime error (message in rp_last_error)              */
 #define RP_ENOMEM (-7)
 #define RP_ENODEV (-8)    /* operation needs a GPU but the context is host-only         */
+#define RP_EAGAIN (-9)    /* random GG: the worker's group waits in the pending queue
+                             (P:728-733); call rp_group_generate again                  */
 
 /* ---- configuration ----------------------------------------------------------- */
 #define RP_FLAG_TRACE 0x1       /* keep the JSONL decision trace (rp_trace_open)       */
@@ -71,6 +73,9 @@ extern "C" {
                                    rank 0, mapped by the others), serialized by a
                                    process-shared mutex; cross-GPU groups may then be
                                    issued outside batches (launched in GG order)       */
+#define RP_FLAG_RANDOM_GG 0x8   /* the basic GG of §4.1 instead of GB + GD:
+                                   a random group containing the requester, the lock
+                                   vector, a FIFO pending queue; k = 2 is AD-PSGD       */
 
 #define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
 #define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */
@@ -110,7 +115,9 @@ typedef struct rp_stats {
   int64_t max_gb_depth;       /* deepest Group Buffer seen                              */
   int64_t lock_assertions;    /* conflict checks performed                              */
   int64_t bytes_hbm;          /* algorithmic HBM bytes moved by launched parts          */
-  int64_t bytes_nvlink;       /* algorithmic NVLink bytes read by this GPU              */
+  int64_t bytes_nvlink;       /* algorithmic NVLink bytes stored by this GPU            */
+  int64_t gg_pending;         /* random GG: requests whose group had to wait (conflicts) */
+  int64_t gg_granted;         /* random GG: groups granted                              */
 } rp_stats;
 
 /* Device time of this context's P-Reduce kernel launches (RP_FLAG_TIMING),
@@ -207,6 +214,10 @@ int rp_schedule_static_worker(rp_ctx* ctx, int32_t rule, int64_t step, int32_t w
  * w's Group Buffer is non-empty return its head, else run a Global Division
  * over workers with empty GB, passing the slowdown filter and not retired,
  * push the groups to their members' GBs (lock bits set) and return w's.
+ * With RP_FLAG_RANDOM_GG (§4.1): serve the group w was notified of, else draw
+ * a random group containing w; if a member's lock bit is set the group waits
+ * in the pending queue and the call returns RP_EAGAIN (*out = that group) —
+ * call again (a retry does not count as a new request).
  * Serialized by an internal mutex; appends {"ev":"req"} to the trace.
  * Errors: RP_ESTATE (w still holds an unfinished group, or w retired), RP_EINVAL.
  * Multi-process jobs: every rank runs the same deterministic GG; lockstep

@@ -161,3 +161,143 @@ class GroupGenerator:
 
     def gb_depth(self):
         return max(len(b) for b in self.s.gb)
+
+
+class RandomGroupGenerator:
+    """The basic GG of §4.1: random groups, lock vector, pending group queue.
+
+    TEST INFRASTRUCTURE ONLY. Steps, in the paper's protocol order:
+      * a worker's request: if the GG already notified it of a granted group
+        (its inbox, the per-worker queue of P:705 "notifies the workers"), serve that;
+      * otherwise "randomly generates a group" containing the initiator:
+        the initiator plus k-1 distinct others drawn uniformly (splitmix64 Fisher-Yates over
+        the non-retired workers, first k-1; reading R8);
+      * "sets the corresponding bits in the lock vector" if none is set and notifies the
+        members; a group overlapping a held lock is "blocked ... in a pending
+        group queue" (P:728-733) and the initiator waits;
+      * on the ack after P-Reduce the bits are released and the pending queue is rescanned
+        in FIFO order; newly unblocked groups are granted.
+    Readings (R21-R22): a waiting initiator's repeated request is a retry (its
+    counter is not incremented again) and is served any group it was notified of first; a
+    pending group that contains a retired worker is cancelled and its initiator draws again.
+    AD-PSGD is the k = 2 special case.
+    """
+
+    def __init__(self, n, k, seed_gd=3):
+        if not (1 <= k <= n):
+            raise ValueError("need 1 <= k <= n")
+        self.n, self.k = n, k
+        self.rng = seed_gd & _MASK
+        self.seq = 0
+        self.lock = 0
+        self.retired = 0
+        self.retiring = 0
+        self.inbox = [[] for _ in range(n)]
+        self.pending = []                 # FIFO of seq
+        self.pending_of = [-1] * n        # pending group initiated by w
+        self.waiting = [False] * n
+        self.handed = [-1] * n
+        self.groups = {}                  # seq -> members (granted or pending)
+        self.initiator = {}
+        self.counters = [0] * n
+        self.trace = []
+        self.n_pending = 0
+        self.n_granted = 0
+
+    def _next(self):
+        self.rng = (self.rng + 0x9E3779B97F4A7C15) & _MASK
+        return _mix(self.rng)
+
+    def _bits(self, members):
+        b = 0
+        for m in members:
+            b |= 1 << m
+        return b
+
+    def _grant(self, seq):
+        members = self.groups[seq]
+        self.lock |= self._bits(members)
+        for m in members:
+            self.inbox[m].append(seq)
+        self.n_granted += 1
+
+    def req(self, i, members=None):
+        """Returns ("ok", seq, members) or ("pending", seq, members). `members` (tests only)
+        replaces the random draw, to replay the paper's walk-through."""
+        if not (0 <= i < self.n) or (self.retired >> i) & 1:
+            raise ProtocolError(f"request from invalid or retired worker {i}")
+        if self.handed[i] != -1:
+            raise ProtocolError(f"worker {i} requested again before its group {self.handed[i]} completed")
+        if not self.waiting[i]:
+            self.counters[i] += 1
+        if self.inbox[i]:
+            seq = self.inbox[i][0]
+            self.handed[i] = seq
+            self.waiting[i] = False
+            self.trace.append(("req", i, "ok", seq))
+            return "ok", seq, self.groups[seq]
+        if self.pending_of[i] != -1:
+            self.waiting[i] = True
+            self.trace.append(("req", i, "pending", self.pending_of[i]))
+            return "pending", self.pending_of[i], self.groups[self.pending_of[i]]
+        if members is None:
+            cand = [v for v in range(self.n) if v != i and not (self.retired >> v) & 1]
+            for q in range(len(cand) - 1, 0, -1):  # Fisher-Yates, as in GD
+                j = self._next() % (q + 1)
+                cand[q], cand[j] = cand[j], cand[q]
+            members = [i] + cand[:self.k - 1]
+        members = tuple(sorted(members))
+        seq = self.seq
+        self.seq += 1
+        self.groups[seq] = members
+        self.initiator[seq] = i
+        if self.lock & self._bits(members):      # conflict: serialize (P:728-733)
+            self.pending.append(seq)
+            self.pending_of[i] = seq
+            self.waiting[i] = True
+            self.n_pending += 1
+            self.trace.append(("req", i, "pending", seq))
+            return "pending", seq, members
+        self._grant(seq)
+        self.handed[i] = seq
+        self.waiting[i] = False
+        self.trace.append(("req", i, "ok", seq))
+        return "ok", seq, members
+
+    def _rescan(self):
+        for seq in list(self.pending):
+            members = self.groups[seq]
+            ini = self.initiator[seq]
+            if self.retired & self._bits(members):          # reading R22: cancel
+                self.pending.remove(seq)
+                self.pending_of[ini] = -1
+                del self.groups[seq]
+                continue
+            if not (self.lock & self._bits(members)):
+                self.pending.remove(seq)
+                self.pending_of[ini] = -1
+                self._grant(seq)
+
+    def done(self, seq):
+        members = self.groups[seq]
+        for m in members:
+            if not self.inbox[m] or self.inbox[m][0] != seq or self.handed[m] != seq:
+                raise ProtocolError(f"group {seq} completed out of protocol at worker {m}")
+        for m in members:
+            self.inbox[m].pop(0)
+            self.handed[m] = -1
+            self.lock &= ~(1 << m)
+            if (self.retiring >> m) & 1:
+                self.retiring &= ~(1 << m)
+                self.retired |= 1 << m
+        del self.groups[seq]
+        self.trace.append(("done", seq))
+        self._rescan()
+        return members
+
+    def retire(self, w):
+        if self.handed[w] != -1:
+            self.retiring |= 1 << w
+        else:
+            self.retired |= 1 << w
+            self._rescan()

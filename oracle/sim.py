@@ -22,7 +22,7 @@ import numpy as np
 
 from rp_inputs import gen as xi_mod
 from . import schedule as sched_mod
-from .gg import GroupGenerator, ProtocolError
+from .gg import GroupGenerator, ProtocolError, RandomGroupGenerator
 from .update import fused_group_update
 
 F32 = np.float32
@@ -73,26 +73,35 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
 
 
 def replay_trace(events, n, n_params, *, k, c_thres, seed_gd, lr=0.1,
-                 workers_per_gpu=None, lo=0, hi=None):
+                 workers_per_gpu=None, lo=0, hi=None, policy="gd"):
     """Replay an async decision trace; returns (X, steps_per_worker).
 
     events: iterable of dicts {"ev": "req", "w", "seq", "members"} |
-            {"ev": "done", "seq"} | {"ev": "retire", "w"} in GG order.
+            {"ev": "done", "seq"} | {"ev": "retire", "w"} in GG order; with the random GG
+            (policy "random") a blocked request is {"ev": "req", "w", "pending": seq}.
     Raises ProtocolError if a recorded grant differs from the oracle GG's.
     """
     hi = n_params if hi is None else hi
     X = init_replicas(n, n_params, lo, hi)
     wpg = workers_per_gpu or n
-    gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd)
+    gg = (GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd) if policy == "gd"
+          else RandomGroupGenerator(n, k, seed_gd=seed_gd))
     t_of = [0] * n
     for e in events:
-        if e["ev"] == "req":
+        if e["ev"] == "req" and policy == "random":
+            status, seq, members = gg.req(e["w"])
+            want = ("pending", e["pending"]) if "pending" in e else ("ok", e["seq"])
+            if (status, seq) != want or ("members" in e and tuple(members) != tuple(e["members"])):
+                raise ProtocolError(f"decision mismatch at req w={e['w']}: oracle {status} {seq}:{members} "
+                                    f"vs trace {e}")
+        elif e["ev"] == "req":
             seq, members = gg.req(e["w"])
             if seq != e["seq"] or tuple(members) != tuple(e["members"]):
                 raise ProtocolError(f"grant mismatch at req w={e['w']}: oracle {seq}:{members} "
                                     f"vs trace {e['seq']}:{e['members']}")
         elif e["ev"] == "done":
             members = gg.done(e["seq"])
+            members = tuple(members)
             G = {}
             for w in members:
                 t_of[w] += 1

@@ -8,7 +8,9 @@ global barrier (P:485-487):
             s * T_c), or rp_compute_delay on the worker's stream (device busy wait)
   Step 2    rp_step(w, g, lr)
   Step 3    rp_group_generate(w): Group Buffer head or a Global Division over the
-            idle workers that pass the slowdown filter
+            idle workers that pass the slowdown filter (P:997-1067, P:1181-1195);
+            or, with policy="random", the basic GG of §4.1 (random group, lock vector,
+            pending queue: the request is retried while the group waits)
   Step 4    rp_preduce(w, G) + rp_barrier_free_wait(w) (host wait, group-local)
 
 With several GPUs (one process each) the contexts share ONE Group Generator in
@@ -33,13 +35,18 @@ def _ceil_to(v, m):
 
 class AsyncRunner:
     def __init__(self, world, n_params, *, group_size, c_thres=4, seed_gd=3, n_gpus=1, rank=0, device=None,
-                 lr=0.1, job_id=0, peer_group=None, trace_path=None, grad_mode="per_step", flags=0):
+                 lr=0.1, job_id=0, peer_group=None, trace_path=None, grad_mode="per_step", flags=0,
+                 policy="gd"):
         if grad_mode not in ("per_step", "resident"):
             raise ValueError("grad_mode must be 'per_step' or 'resident'")
         self.device = rank if device is None else device
         torch.cuda.set_device(self.device)
         if n_gpus > 1:
             flags |= RP_FLAG_SHARED_GG
+        if policy == "random":          # §4.1 random GG (k = 2: AD-PSGD)
+            flags |= rp.RP_FLAG_RANDOM_GG
+        elif policy != "gd":
+            raise ValueError("policy must be 'gd' or 'random'")
         self.world, self.n, self.lr, self.grad_mode = world, n_params, lr, grad_mode
         self.n_gpus, self.peer_group = n_gpus, peer_group
         self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device, group_size=group_size,
@@ -96,7 +103,7 @@ class AsyncRunner:
                     if self.grad_mode == "per_step":
                         rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, s)
                     self.ctx.step(w, None, self.lr)
-                    g = self.ctx.group_generate(w)
+                    g = self.ctx.group_generate_wait(w)    # random GG: retry while pending
                     if final:
                         self.ctx.retire(w)
                     self.ctx.preduce(w, g)

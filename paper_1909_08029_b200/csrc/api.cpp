@@ -544,7 +544,8 @@ int open_shared_gg(rp_ctx* c) {
     pthread_mutex_init(&c->shm->mu, &at);
     pthread_mutexattr_destroy(&at);
     c->shm->trace_n = 0;
-    rp::gg_init(&c->shm->gg, k.world, k.group_size, k.c_thres, k.seed_gd);
+    rp::gg_init(&c->shm->gg, k.world, k.group_size, k.c_thres, k.seed_gd,
+                (k.flags & RP_FLAG_RANDOM_GG) ? rp::kPolicyRandom : rp::kPolicyGD);
     __atomic_store_n(&c->shm->magic, kSharedMagic, __ATOMIC_RELEASE);
   } else {
     const auto t0 = std::chrono::steady_clock::now();
@@ -596,6 +597,7 @@ const char* rp_strerror(int status) {
     case RP_ECUDA: return "CUDA error";
     case RP_ENOMEM: return "out of memory";
     case RP_ENODEV: return "no GPU in this context";
+    case RP_EAGAIN: return "group pending (retry)";
     default: return "unknown status";
   }
 }
@@ -618,7 +620,8 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
   if (!c) return fail(RP_ENOMEM, "rp_init: allocation failed");
   c->cfg = k;
   if (c->cfg.workers_per_gpu < 1) c->cfg.workers_per_gpu = k.world;
-  rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd);
+  const int policy = (k.flags & RP_FLAG_RANDOM_GG) ? rp::kPolicyRandom : rp::kPolicyGD;
+  rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd, policy);
   if (k.flags & RP_FLAG_SHARED_GG) {
     const int rc = open_shared_gg(c);
     if (rc != RP_OK) {
@@ -892,6 +895,11 @@ int rp_group_generate(rp_ctx* c, int32_t w, rp_group* out) {
   std::lock_guard<std::mutex> lk(c->mu);
   GGLock gl(c);
   const int rc = rp::gg_request(c->ggp, w, out);
+  if (rc == RP_EAGAIN) {
+    trace_line(c, "\"ev\":\"req\",\"w\":" + std::to_string(w) + ",\"pending\":" + std::to_string(out->seq));
+    return fail(RP_EAGAIN, "group " + std::to_string(out->seq) + " of worker " + std::to_string(w) +
+                               " waits in the pending queue");
+  }
   if (rc != RP_OK) return rc;
   c->stats.gg_requests++;
   trace_line(c, "\"ev\":\"req\",\"w\":" + std::to_string(w) + "," + group_json(*out));
@@ -1137,6 +1145,8 @@ int rp_stats_get(rp_ctx* c, rp_stats* out) {
   GGLock gl(c);
   out->gd_calls = c->ggp->gd_calls;
   out->max_gb_depth = c->ggp->max_depth;
+  out->gg_pending = c->ggp->n_pending;
+  out->gg_granted = c->ggp->n_granted;
   return RP_OK;
 }
 

@@ -38,15 +38,128 @@ GGGroup* find_slot(GGState* s, int64_t seq) {
 }
 }  // namespace
 
-void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed) {
+void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy) {
   std::memset(s, 0, sizeof(*s));
   s->n = n;
   s->k = k;
   s->c_thres = c_thres;
   s->rng = seed;
-  for (int w = 0; w < RP_MAX_WORLD; ++w) s->handed[w] = -1;
+  s->policy = policy;
+  for (int w = 0; w < RP_MAX_WORLD; ++w) {
+    s->handed[w] = -1;
+    s->pending_of[w] = -1;
+  }
   for (auto& g : s->table) g.seq = -1;
 }
+
+namespace {
+void fill_out(const GGGroup* g, rp_group* out) {
+  out->seq = g->seq;
+  out->size = g->size;
+  for (int t = 0; t < RP_MAX_GROUP; ++t) out->members[t] = t < g->size ? g->members[t] : -1;
+}
+uint64_t member_bits(const GGGroup* g) {
+  uint64_t b = 0;
+  for (int t = 0; t < g->size; ++t) b |= 1ull << g->members[t];
+  return b;
+}
+// random GG: lock the group's members and notify them (their inbox = GB)
+int grant(GGState* s, GGGroup* g) {
+  for (int t = 0; t < g->size; ++t)
+    if (s->gb_len[g->members[t]] >= kGbCap) return fail(RP_ESTATE, "inbox overflow");
+  s->lock |= member_bits(g);
+  g->granted = 1;
+  for (int t = 0; t < g->size; ++t) {
+    const int m = g->members[t];
+    s->gb[m][s->gb_len[m]++] = g->seq;
+    s->max_depth = std::max<int64_t>(s->max_depth, s->gb_len[m]);
+  }
+  s->n_granted++;
+  return RP_OK;
+}
+// after a release, rescan the pending queue in FIFO order; a pending group with a
+// retired member is cancelled and its initiator draws again (reading R22).
+void rescan(GGState* s) {
+  int keep = 0;
+  for (int q = 0; q < s->npending; ++q) {
+    GGGroup* g = find_slot(s, s->pending[q]);
+    if (!g) continue;
+    const uint64_t bits = member_bits(g);
+    if (s->retired & bits) {
+      s->pending_of[g->initiator] = -1;
+      g->seq = -1;
+      continue;
+    }
+    if (!(s->lock & bits) && grant(s, g) == RP_OK) {
+      s->pending_of[g->initiator] = -1;
+      continue;
+    }
+    s->pending[keep++] = s->pending[q];
+  }
+  s->npending = keep;
+}
+
+// The basic GG of §4.1: serve a notified group, else draw a random group
+// containing w (splitmix64 Fisher-Yates, first k-1 others); grant it if no member's lock
+// bit is set, otherwise queue it and let w retry.
+int random_request(GGState* s, int w, rp_group* out) {
+  if (!s->waiting[w]) {
+    s->requests++;
+    s->counters[w] += 1;
+  }
+  if (s->gb_len[w] > 0) {
+    const GGGroup* g = gg_find(s, s->gb[w][0]);
+    if (!g) return fail(RP_ESTATE, "inbox head not in table");
+    s->handed[w] = g->seq;
+    s->waiting[w] = 0;
+    fill_out(g, out);
+    return RP_OK;
+  }
+  if (s->pending_of[w] >= 0) {
+    const GGGroup* g = gg_find(s, s->pending_of[w]);
+    if (!g) return fail(RP_ESTATE, "pending group not in table");
+    s->waiting[w] = 1;
+    fill_out(g, out);
+    return RP_EAGAIN;
+  }
+  int cand[RP_MAX_WORLD];
+  int nc = 0;
+  for (int v = 0; v < s->n; ++v)
+    if (v != w && !((s->retired >> v) & 1)) cand[nc++] = v;
+  for (int q = nc - 1; q >= 1; --q) {
+    const int j = static_cast<int>(next_rand(s) % static_cast<uint64_t>(q + 1));
+    std::swap(cand[q], cand[j]);
+  }
+  int members[RP_MAX_GROUP];
+  int sz = 0;
+  members[sz++] = w;
+  for (int t = 0; t < std::min(s->k - 1, nc); ++t) members[sz++] = cand[t];
+  std::sort(members, members + sz);
+  GGGroup* slot = find_slot(s, -1);
+  if (!slot) return fail(RP_ENOMEM, "GG group table full");
+  slot->seq = s->next_seq++;
+  slot->size = sz;
+  slot->arrived = 0;
+  slot->ticket = -1;
+  slot->initiator = w;
+  slot->granted = 0;
+  for (int t = 0; t < sz; ++t) slot->members[t] = members[t];
+  fill_out(slot, out);
+  if (s->lock & member_bits(slot)) {  // conflict: serialize
+    if (s->npending >= kTableCap) return fail(RP_ENOMEM, "pending queue full");
+    s->pending[s->npending++] = slot->seq;
+    s->pending_of[w] = slot->seq;
+    s->waiting[w] = 1;
+    s->n_pending++;
+    return RP_EAGAIN;
+  }
+  const int rc = grant(s, slot);
+  if (rc != RP_OK) return rc;
+  s->handed[w] = slot->seq;
+  s->waiting[w] = 0;
+  return RP_OK;
+}
+}  // namespace
 
 const GGGroup* gg_find(const GGState* s, int64_t seq) {
   for (const auto& g : s->table)
@@ -106,6 +219,7 @@ int gg_request(GGState* s, int w, rp_group* out) {
   if (s->handed[w] != -1)
     return fail(RP_ESTATE, "gg_request: worker " + std::to_string(w) + " still holds group " +
                                std::to_string(s->handed[w]));
+  if (s->policy == kPolicyRandom) return random_request(s, w, out);
   s->requests++;
   s->counters[w] += 1;  // reading R10: counted at request time
   if (s->gb_len[w] == 0) {
@@ -151,15 +265,18 @@ int gg_done(GGState* s, int64_t seq, rp_group* released) {
     }
   }
   g->seq = -1;
+  if (s->policy == kPolicyRandom) rescan(s);
   return RP_OK;
 }
 
 int gg_retire(GGState* s, int w) {
   if (w < 0 || w >= s->n) return fail(RP_EINVAL, "gg_retire: worker out of range");
-  if (s->handed[w] != -1)
+  if (s->handed[w] != -1) {
     s->retiring |= 1ull << w;
-  else
+  } else {
     s->retired |= 1ull << w;
+    if (s->policy == kPolicyRandom) rescan(s);
+  }
   return RP_OK;
 }
 

@@ -27,7 +27,12 @@ struct GGGroup {
   int32_t members[RP_MAX_GROUP];
   uint64_t arrived;  // members that called rp_preduce (shared GG, any process)
   int64_t ticket;    // order of complete arrival (shared GG), -1 until all members arrived
+  int32_t initiator; // random GG: the requesting worker
+  int32_t granted;   // random GG: lock bits held (0 while in the pending queue)
 };
+
+constexpr int32_t kPolicyGD = 0;      // Group Buffer + Global Division + filter (§5)
+constexpr int32_t kPolicyRandom = 1;  // random groups + lock vector + pending queue (§4.1)
 
 // Plain-old-data so it can live in process-shared memory.
 struct GGState {
@@ -43,10 +48,18 @@ struct GGState {
   GGGroup table[kTableCap];
   int64_t gd_calls, requests, max_depth;
   int64_t next_ticket;            // complete-arrival order of groups (shared GG)
+  // random GG (§4.1)
+  int32_t policy;
+  int32_t npending;
+  int64_t pending[kTableCap];     // FIFO of pending group seqs
+  int64_t pending_of[RP_MAX_WORLD];
+  uint8_t waiting[RP_MAX_WORLD];
+  int64_t n_pending, n_granted;
 };
 
-void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed);
-// Returns RP_OK and fills *out, or an RP_E* code.
+void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy = kPolicyGD);
+// Returns RP_OK and fills *out, RP_EAGAIN (random GG: the worker's group waits in the
+// pending queue; *out holds it; call again), or an RP_E* code.
 int gg_request(GGState* s, int w, rp_group* out);
 // Group `seq` completed: pop it from its members' GBs, clear lock bits.
 int gg_done(GGState* s, int64_t seq, rp_group* released);

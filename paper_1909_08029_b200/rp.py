@@ -19,12 +19,14 @@ RP_ETIMEOUT = -5
 RP_ECUDA = -6
 RP_ENOMEM = -7
 RP_ENODEV = -8
+RP_EAGAIN = -9
 
 RP_MAX_WORLD = 64
 RP_MAX_GROUP = 16
 RP_FLAG_TRACE = 0x1
 RP_FLAG_TIMING = 0x2
 RP_FLAG_SHARED_GG = 0x4
+RP_FLAG_RANDOM_GG = 0x8
 RP_SCHED_PAPER4 = 1
 RP_SCHED_SHIFT_K = 2
 RP_WAIT_DEVICE = -1
@@ -81,7 +83,8 @@ class rp_group(ctypes.Structure):
 class rp_stats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "groups_launched", "singleton_groups", "cross_gpu_groups", "kernel_launches", "gd_calls",
-        "gg_requests", "max_gb_depth", "lock_assertions", "bytes_hbm", "bytes_nvlink")]
+        "gg_requests", "max_gb_depth", "lock_assertions", "bytes_hbm", "bytes_nvlink", "gg_pending",
+        "gg_granted")]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -257,7 +260,11 @@ def rp_schedule_static_worker(ctx, rule, step, w):
 
 def rp_group_generate(ctx, w):
     g = rp_group()
-    _check(load_library().rp_group_generate(ctx, w, ctypes.byref(g)), "rp_group_generate")
+    try:
+        _check(load_library().rp_group_generate(ctx, w, ctypes.byref(g)), "rp_group_generate")
+    except RPError as e:
+        e.group = g            # RP_EAGAIN: the group waiting in the pending queue
+        raise
     return g
 
 
@@ -404,6 +411,18 @@ class Context:
 
     def group_generate(self, w):
         return rp_group_generate(self.handle, w)
+
+    def group_generate_wait(self, w, timeout_s=600.0, poll_s=20e-6):
+        """rp_group_generate, retrying while the random GG keeps the group pending (RP_EAGAIN)."""
+        import time
+        t_end = time.perf_counter() + timeout_s
+        while True:
+            try:
+                return rp_group_generate(self.handle, w)
+            except RPError as e:
+                if e.status != RP_EAGAIN or time.perf_counter() > t_end:
+                    raise
+            time.sleep(poll_s)
 
     def group_generate_many(self, workers):
         return rp_group_generate_many(self.handle, workers)

@@ -107,12 +107,14 @@ def test_disjoint_groups_no_global_barrier():
     ctx.close()
 
 
-@pytest.mark.parametrize("slow", [1, 5])
-def test_async_gd_threads_replay_bit_exact(tmp_path, slow):
-    """cfg 5 semantics on one GPU: one host thread per worker, dynamic GG with GB + GD + filter,
-    worker 0 slowed; the decision trace replays through the oracle to the same bits."""
-    world, n, k, steps, c_thres = 8, 50_000, 3, 12, 2
-    ctx, X, G = _ctx(world, n, group_size=k, c_thres=c_thres, seed_gd=7)
+@pytest.mark.parametrize("slow,policy,k", [(1, "gd", 3), (5, "gd", 3), (2, "random", 3), (2, "random", 2)])
+def test_async_gd_threads_replay_bit_exact(tmp_path, slow, policy, k):
+    """cfg 5 semantics on one GPU: one host thread per worker, dynamic GG (GB + GD + filter, or the
+    random GG of §4.1 with its pending queue; k = 2 is AD-PSGD), worker 0 slowed; the decision
+    trace replays through the oracle to the same bits."""
+    world, n, steps, c_thres = 8, 50_000, 12, 2
+    flags = rp.RP_FLAG_RANDOM_GG if policy == "random" else 0
+    ctx, X, G = _ctx(world, n, group_size=k, c_thres=c_thres, seed_gd=7, flags=flags)
     trace = tmp_path / "trace.jsonl"
     ctx.trace_open(trace)
     errors = []
@@ -126,7 +128,7 @@ def test_async_gd_threads_replay_bit_exact(tmp_path, slow):
                     time.sleep(0.002 * slow)                # heterogeneity injection
                 rp.fill_xi(G[w], n, 2, w, t, 0, s)
                 ctx.step(w, None, 0.1)
-                g = ctx.group_generate(w)
+                g = ctx.group_generate_wait(w)
                 if t == steps:
                     ctx.retire(w)
                 ctx.preduce(w, g)
@@ -142,10 +144,13 @@ def test_async_gd_threads_replay_bit_exact(tmp_path, slow):
     assert not errors, errors
     torch.cuda.synchronize()
     events = [json.loads(ln) for ln in open(trace)]
-    Xo, t_of = sim.replay_trace(events, world, n, k=k, c_thres=c_thres, seed_gd=7)
+    Xo, t_of = sim.replay_trace(events, world, n, k=k, c_thres=c_thres, seed_gd=7, policy=policy)
     assert t_of == [steps] * world
     for w in range(world):
         assert np.array_equal(X[w].cpu().numpy().view(np.uint32), Xo[w].view(np.uint32)), w
     st = ctx.stats()
-    assert st["max_gb_depth"] <= 1 and st["gd_calls"] >= 1
+    if policy == "gd":
+        assert st["max_gb_depth"] <= 1 and st["gd_calls"] >= 1
+    else:
+        assert st["gg_granted"] >= world * steps // k
     ctx.close()

@@ -129,3 +129,47 @@ def test_gg_protocol_errors():
         with pytest.raises(rp.RPError) as e:
             c.group_generate(other[0])
         assert e.value.status == rp.RP_ESTATE
+
+
+@pytest.mark.parametrize("n,k,seed", [(8, 3, 1), (6, 2, 7), (16, 3, 3), (5, 4, 11)])
+def test_random_gg_interleavings_bit_exact(n, k, seed, tmp_path):
+    """The §4.1 random GG (lock vector + pending queue) in C++ vs the oracle, request by request."""
+    from oracle.gg import RandomGroupGenerator
+    rnd = random.Random(seed)
+    og = RandomGroupGenerator(n, k, seed_gd=seed)
+    left = [rnd.randint(2, 8) for _ in range(n)]
+    arrived = {}
+    trace = tmp_path / "trace.jsonl"
+    with rp.Context(n, 1024, n_gpus=0, group_size=k, seed_gd=seed, flags=rp.RP_FLAG_RANDOM_GG) as c:
+        c.trace_open(trace)
+        for _ in range(100000):
+            if not any(left):
+                break
+            full = [q for q, a in arrived.items() if a == set(og.groups[q])]
+            ready = [w for w in range(n) if left[w] and og.handed[w] == -1]
+            if full and (not ready or rnd.random() < 0.5):
+                q = rnd.choice(full)
+                c.gg_release(q)
+                for m in og.done(q):
+                    left[m] -= 1
+                del arrived[q]
+                continue
+            w = rnd.choice(ready)
+            st, seq, mem = og.req(w)
+            if st == "pending":
+                with pytest.raises(rp.RPError) as e:
+                    c.group_generate(w)
+                assert e.value.status == rp.RP_EAGAIN and e.value.group.seq == seq
+                continue
+            g = c.group_generate(w)
+            assert (g.seq, tuple(g.member_list())) == (seq, mem)
+            if left[w] == 1:
+                c.retire(w)
+                og.retire(w)
+            arrived.setdefault(seq, set()).add(w)
+        assert not any(left)
+        st = c.stats()
+        assert st["gg_pending"] == og.n_pending and st["gg_granted"] == og.n_granted
+    events = [json.loads(ln) for ln in open(trace)]
+    from oracle import sim
+    sim.replay_trace(events, n, 16, k=k, c_thres=0, seed_gd=seed, policy="random")
