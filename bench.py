@@ -36,6 +36,10 @@ WORKLOADS = {
     "cfg2": dict(desc="configs[1]: 8 workers per B200, ResNet-50-sized 25.6M fp32, k=3, GB+GD over all "
                       "8*N workers (N=1: exactly configs[1]; N>1: weak scaling of that layout)",
                  wpg=8, n=N_R50, k=3, mode="gd", rule=None),
+    "cfg2ii": dict(desc="configs[1] layout (8 workers per B200, ResNet-50-sized, k=3) with Inter-Intra "
+                        "Synchronization (§5.2, GPU = node): Head Workers across GPUs, the rest per GPU, "
+                        "then whole-GPU groups",
+                   wpg=8, n=N_R50, k=3, mode="gd", rule=None, inter_intra=True),
     "cfg3": dict(desc="configs[2]: 1 worker per B200 (8 workers on 8 GPUs), ResNet-50-sized, k=3, GB+GD, "
                       "concurrent disjoint groups over NVLink",
                  wpg=1, n=N_R50, k=3, mode="gd", rule=None),
@@ -171,9 +175,10 @@ def run_ours(args, wl):
     wpg, n = wl["wpg"], wl["n"]
     world = wpg * n_gpus
     k = min(wl["k"], world)              # e.g. configs[2] at 2 GPUs: 2 workers, groups of 2
+    flags = rp.RP_FLAG_TIMING | (rp.RP_FLAG_INTER_INTRA if wl.get("inter_intra") else 0)
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
-                            rank=rank, device=local_rank, grad_mode="resident", flags=rp.RP_FLAG_TIMING,
-                            peer_group=pg)
+                            rank=rank, device=local_rank, grad_mode="resident", flags=flags,
+                            nodes=n_gpus if wl.get("inter_intra") else 0, peer_group=pg)
     for _ in range(args.warmup):
         runner.step()
     runner.synchronize()
@@ -474,7 +479,8 @@ def oracle_steps(wl, n_gpus, sample, steps):
     X = {w: gen.x0(w, wl["n"], 0, sample) for w in range(world)}
     G = {w: gen.grad(w, 1, wl["n"], 0, sample) for w in range(world)}
     k = min(wl["k"], world)
-    gg = GroupGenerator(world, k, c_thres=4, seed_gd=3) if wl["mode"] in ("gd", "async") else None
+    gg = (GroupGenerator(world, k, c_thres=4, seed_gd=3, nodes=n_gpus if wl.get("inter_intra") else 0)
+          if wl["mode"] in ("gd", "async") else None)
     lr = np.float32(0.1)
     t0 = time.perf_counter()
     for t in range(1, steps + 1):

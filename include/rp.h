@@ -76,6 +76,10 @@ extern "C" {
 #define RP_FLAG_RANDOM_GG 0x8   /* the basic GG of §4.1 instead of GB + GD:
                                    a random group containing the requester, the lock
                                    vector, a FIFO pending queue; k = 2 is AD-PSGD       */
+#define RP_FLAG_INTER_INTRA 0x10 /* §5.2 Inter-Intra Synchronization: every Global
+                                   Division queues an Inter group (Head Workers across
+                                   nodes, the rest node-local) and an Intra group (whole
+                                   node); nodes = cfg.nodes, or n_gpus when 0           */
 
 #define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
 #define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */

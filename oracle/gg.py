@@ -68,23 +68,27 @@ class GGState:
 class GroupGenerator:
     """The GG of §5 with GB + GD + filter; one instance = one serial decision loop."""
 
-    def __init__(self, n, k, c_thres=4, seed_gd=3):
+    def __init__(self, n, k, c_thres=4, seed_gd=3, nodes=0):
+        """nodes > 0: Inter-Intra Synchronization (§5.2) over nodes of n // nodes workers."""
         if not (1 <= k <= n):
             raise ValueError("need 1 <= k <= n")
+        if nodes and n % nodes:
+            raise ValueError("n must be a multiple of nodes")
         self.s = GGState(n=n, k=k, c_thres=c_thres, rng=seed_gd & _MASK,
                          gb=[[] for _ in range(n)], counters=[0] * n, handed=[-1] * n)
         self.trace = []
         self.gd_calls = 0
+        self.nodes = nodes
+        self.head_rot = [0] * max(nodes, 1)
 
     # -- RNG: splitmix64 (next = MIX(state += golden)) -------------------------
     def _next(self):
         self.s.rng = (self.s.rng + 0x9E3779B97F4A7C15) & _MASK
         return _mix(self.s.rng)
 
-    def _global_division(self, i):
-        """P:1032-1067: partition the idle workers (empty GB), initiator's group first."""
+    def _idle(self, i):
+        """Workers a division may assign: empty GB, slowdown filter, not retired (R7)."""
         s = self.s
-        self.gd_calls += 1
         cand = []
         for v in range(s.n):
             if v == i or s.gb[v] or (s.retired >> v) & 1:
@@ -92,24 +96,72 @@ class GroupGenerator:
             if s.c_thres > 0 and not (s.counters[i] - s.counters[v] < s.c_thres):
                 continue  # slowdown filter
             cand.append(v)
+        return cand
+
+    def _shuffle(self, cand):
         for q in range(len(cand) - 1, 0, -1):  # Fisher-Yates
             j = self._next() % (q + 1)
             cand[q], cand[j] = cand[j], cand[q]
-        chunks = [[i] + cand[:s.k - 1]]
-        rest = cand[s.k - 1:]
-        chunks += [rest[p:p + s.k] for p in range(0, len(rest), s.k)]
+        return cand
+
+    def _push(self, chunks):
+        """Create the groups in order and append them to their members' GBs. Lock bit w is
+        held while GB[w] is non-empty; a division may only use workers without one."""
+        s = self.s
+        before = s.lock
         for ch in chunks:
             members = tuple(sorted(ch))
             bits = 0
             for m in members:
                 bits |= 1 << m
-            if s.lock & bits:  # overlapping groups must be serialized
-                raise ConflictError(f"GD produced a group overlapping a held lock: {members}")
+            if before & bits:  # P:690-692: overlapping groups must be serialized
+                raise ConflictError(f"division produced a group overlapping a held lock: {members}")
             s.lock |= bits
             s.groups[s.seq] = members
             for m in members:
                 s.gb[m].append(s.seq)
             s.seq += 1
+
+    def _global_division(self, i):
+        """P:1032-1067: partition the idle workers (empty GB), initiator's group first."""
+        s = self.s
+        self.gd_calls += 1
+        if self.nodes:
+            return self._inter_intra_division(i)
+        cand = self._shuffle(self._idle(i))
+        chunks = [[i] + cand[:s.k - 1]]
+        rest = cand[s.k - 1:]
+        chunks += [rest[p:p + s.k] for p in range(0, len(rest), s.k)]
+        self._push(chunks)
+
+    def _inter_intra_division(self, i):
+        """§5.2 Inter-Intra Synchronization realized as two divisions.
+
+        Inter phase: one Head Worker per node "randomly divided into several groups"
+        across nodes; the other workers "randomly assigned to groups with only local workers".
+        Intra phase: "a P-Reduce among all the workers in the same node". Both groups go to
+        every worker's GB, Inter first. Readings (R23): over the idle
+        set of the division; heads rotate per node (round-robin over the node's idle workers
+        in ascending order); groups of k, the last one of a list shorter.
+        """
+        s = self.s
+        m = s.n // self.nodes
+        idle = sorted(self._idle(i) + [i])
+        per_node = [[v for v in idle if v // m == a] for a in range(self.nodes)]
+        heads = []
+        for a, ws in enumerate(per_node):
+            if ws:
+                heads.append(ws[self.head_rot[a] % len(ws)])
+                self.head_rot[a] += 1
+        chunks = []
+        hs = self._shuffle(list(heads))
+        chunks += [hs[p:p + s.k] for p in range(0, len(hs), s.k)]
+        for ws in per_node:
+            loc = self._shuffle([v for v in ws if v not in heads])
+            chunks += [loc[p:p + s.k] for p in range(0, len(loc), s.k)]
+        inter = chunks
+        intra = [ws for ws in per_node if ws]
+        self._push(inter + intra)
 
     def req(self, i):
         """Synchronization request of worker i. Returns (seq, members)."""
@@ -137,7 +189,8 @@ class GroupGenerator:
                 raise ProtocolError(f"group {seq} completed before member {m} requested it")
             s.gb[m].pop(0)
             s.handed[m] = -1
-            s.lock &= ~(1 << m)
+            if not s.gb[m]:
+                s.lock &= ~(1 << m)
         self.trace.append(("done", seq))
         for m in members:  # retire atomically with the completion (reading R19)
             if (s.retiring >> m) & 1:

@@ -34,10 +34,11 @@ def init_replicas(n, n_params, lo=0, hi=None):
 
 def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
                  rule=None, k=None, nodes=None, m=None, c_thres=4, seed_gd=3,
-                 lo=0, hi=None, X=None, first_step=1, gg=None, log=None):
+                 lo=0, hi=None, X=None, first_step=1, gg=None, log=None, ii_nodes=0):
     """Simulate `steps` lockstep steps; returns (X, log).
 
-    mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter).
+    mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter; ii_nodes > 0
+    makes every division Inter-Intra, §5.2).
     [lo, hi) restricts the simulated element range (elementwise method, so a
     slice is computed exactly as in the full run).
     log: list receiving (t, [groups]) per step, groups as sorted tuples.
@@ -47,7 +48,7 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
     wpg = workers_per_gpu or n
     log = [] if log is None else log
     if mode == "gd" and gg is None:
-        gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd)
+        gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd, nodes=ii_nodes)
     for t in range(first_step, first_step + steps):
         if mode == "static":
             groups = [tuple(g) for g in sched_mod.groups_for(rule, t, n=n, k=k, nodes=nodes, m=m)]
@@ -73,7 +74,7 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
 
 
 def replay_trace(events, n, n_params, *, k, c_thres, seed_gd, lr=0.1,
-                 workers_per_gpu=None, lo=0, hi=None, policy="gd"):
+                 workers_per_gpu=None, lo=0, hi=None, policy="gd", ii_nodes=0):
     """Replay an async decision trace; returns (X, steps_per_worker).
 
     events: iterable of dicts {"ev": "req", "w", "seq", "members"} |
@@ -84,7 +85,7 @@ def replay_trace(events, n, n_params, *, k, c_thres, seed_gd, lr=0.1,
     hi = n_params if hi is None else hi
     X = init_replicas(n, n_params, lo, hi)
     wpg = workers_per_gpu or n
-    gg = (GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd) if policy == "gd"
+    gg = (GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd, nodes=ii_nodes) if policy == "gd"
           else RandomGroupGenerator(n, k, seed_gd=seed_gd))
     t_of = [0] * n
     for e in events:

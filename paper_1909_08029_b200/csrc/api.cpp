@@ -544,8 +544,7 @@ int open_shared_gg(rp_ctx* c) {
     pthread_mutex_init(&c->shm->mu, &at);
     pthread_mutexattr_destroy(&at);
     c->shm->trace_n = 0;
-    rp::gg_init(&c->shm->gg, k.world, k.group_size, k.c_thres, k.seed_gd,
-                (k.flags & RP_FLAG_RANDOM_GG) ? rp::kPolicyRandom : rp::kPolicyGD);
+    rp::gg_init(&c->shm->gg, k.world, k.group_size, k.c_thres, k.seed_gd, c->gg.policy, c->gg.nodes);
     __atomic_store_n(&c->shm->magic, kSharedMagic, __ATOMIC_RELEASE);
   } else {
     const auto t0 = std::chrono::steady_clock::now();
@@ -621,7 +620,15 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
   c->cfg = k;
   if (c->cfg.workers_per_gpu < 1) c->cfg.workers_per_gpu = k.world;
   const int policy = (k.flags & RP_FLAG_RANDOM_GG) ? rp::kPolicyRandom : rp::kPolicyGD;
-  rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd, policy);
+  int ii_nodes = 0;
+  if (k.flags & RP_FLAG_INTER_INTRA) {
+    ii_nodes = k.nodes > 0 ? k.nodes : k.n_gpus;
+    if (ii_nodes < 1 || k.world % ii_nodes != 0 || policy != rp::kPolicyGD) {
+      delete c;
+      return fail(RP_EINVAL, "rp_init: Inter-Intra needs world = nodes * m (cfg.nodes or n_gpus) and GD");
+    }
+  }
+  rp::gg_init(&c->gg, k.world, k.group_size, k.c_thres, k.seed_gd, policy, ii_nodes);
   if (k.flags & RP_FLAG_SHARED_GG) {
     const int rc = open_shared_gg(c);
     if (rc != RP_OK) {

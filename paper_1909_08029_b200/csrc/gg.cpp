@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <sstream>
+#include <vector>
 
 #include "rp_internal.h"
 
@@ -38,13 +39,14 @@ GGGroup* find_slot(GGState* s, int64_t seq) {
 }
 }  // namespace
 
-void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy) {
+void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy, int nodes) {
   std::memset(s, 0, sizeof(*s));
   s->n = n;
   s->k = k;
   s->c_thres = c_thres;
   s->rng = seed;
   s->policy = policy;
+  s->nodes = nodes;
   for (int w = 0; w < RP_MAX_WORLD; ++w) {
     s->handed[w] = -1;
     s->pending_of[w] = -1;
@@ -167,33 +169,27 @@ const GGGroup* gg_find(const GGState* s, int64_t seq) {
   return nullptr;
 }
 
-static int global_division(GGState* s, int i) {
-  s->gd_calls++;
-  int cand[RP_MAX_WORLD];
-  int nc = 0;
-  for (int v = 0; v < s->n; ++v) {
-    if (v == i || s->gb_len[v] > 0 || ((s->retired >> v) & 1)) continue;
-    if (s->c_thres > 0 && !(s->counters[i] - s->counters[v] < s->c_thres)) continue;  // P:1189
-    cand[nc++] = v;
-  }
-  for (int q = nc - 1; q >= 1; --q) {  // Fisher-Yates
+namespace {
+void shuffle(GGState* s, int* v, int n) {  // Fisher-Yates with the GG's splitmix64 stream
+  for (int q = n - 1; q >= 1; --q) {
     const int j = static_cast<int>(next_rand(s) % static_cast<uint64_t>(q + 1));
-    std::swap(cand[q], cand[j]);
+    std::swap(v[q], v[j]);
   }
-  // chunks: [i] + cand[0:k-1], then consecutive chunks of k
-  int pos = 0;
-  bool first = true;
-  while (first || pos < nc) {
+}
+
+// Create the groups of one division in order and append them to their members' GBs.
+// Lock bit w is held while GB[w] is non-empty; a division may only use workers without one.
+int push_groups(GGState* s, const std::vector<std::vector<int>>& chunks) {
+  const uint64_t before = s->lock;
+  for (const auto& ch : chunks) {
     int members[RP_MAX_GROUP];
-    int sz = 0;
-    if (first) members[sz++] = i;
-    const int take = std::min(first ? s->k - 1 : s->k, nc - pos);
-    for (int t = 0; t < take; ++t) members[sz++] = cand[pos++];
-    first = false;
+    const int sz = static_cast<int>(ch.size());
+    if (sz < 1 || sz > RP_MAX_GROUP) return fail(RP_EINVAL, "division group size out of range");
+    for (int t = 0; t < sz; ++t) members[t] = ch[t];
     std::sort(members, members + sz);
     uint64_t bits = 0;
     for (int t = 0; t < sz; ++t) bits |= 1ull << members[t];
-    if (s->lock & bits) return fail(RP_ECONFLICT, "GD produced a group overlapping a held lock");
+    if (before & bits) return fail(RP_ECONFLICT, "division produced a group overlapping a held lock");
     GGGroup* slot = find_slot(s, -1);
     if (!slot) return fail(RP_ENOMEM, "GG group table full");
     for (int t = 0; t < sz; ++t)
@@ -203,6 +199,8 @@ static int global_division(GGState* s, int i) {
     slot->size = sz;
     slot->arrived = 0;
     slot->ticket = -1;
+    slot->initiator = -1;
+    slot->granted = 1;
     for (int t = 0; t < sz; ++t) {
       const int m = members[t];
       slot->members[t] = m;
@@ -211,6 +209,79 @@ static int global_division(GGState* s, int i) {
     }
   }
   return RP_OK;
+}
+
+void chunk_into(std::vector<std::vector<int>>* out, const int* v, int n, int k) {
+  for (int p = 0; p < n; p += k) out->emplace_back(v + p, v + std::min(n, p + k));
+}
+}  // namespace
+
+static int global_division(GGState* s, int i) {
+  s->gd_calls++;
+  int cand[RP_MAX_WORLD];
+  int nc = 0;
+  for (int v = 0; v < s->n; ++v) {
+    if (v == i || s->gb_len[v] > 0 || ((s->retired >> v) & 1)) continue;
+    if (s->c_thres > 0 && !(s->counters[i] - s->counters[v] < s->c_thres)) continue;  // P:1189
+    cand[nc++] = v;
+  }
+  std::vector<std::vector<int>> chunks;
+  if (s->nodes <= 0) {
+    // [i] + cand[0:k-1], then consecutive chunks of k (reading R8)
+    shuffle(s, cand, nc);
+    std::vector<int> first{i};
+    for (int t = 0; t < std::min(s->k - 1, nc); ++t) first.push_back(cand[t]);
+    chunks.push_back(first);
+    const int used = std::min(s->k - 1, nc);
+    chunk_into(&chunks, cand + used, nc - used, s->k);
+    return push_groups(s, chunks);
+  }
+  // §5.2 Inter-Intra Synchronization as two rounds of one division (reading
+  // R23): Inter = one Head Worker per node (rotating over the node's idle workers, ascending)
+  // grouped across nodes at random, the other idle workers grouped with their own node;
+  // Intra = one group of the node's idle workers per node. Inter groups precede Intra groups
+  // in every GB.
+  int idle[RP_MAX_WORLD];
+  int ni = 0;
+  for (int v = 0; v < s->n; ++v) {
+    bool in = v == i;
+    for (int t = 0; t < nc && !in; ++t) in = cand[t] == v;
+    if (in) idle[ni++] = v;
+  }
+  const int m = s->n / s->nodes;
+  int heads[RP_MAX_WORLD];
+  int nh = 0;
+  uint64_t head_bits = 0;
+  for (int a = 0; a < s->nodes; ++a) {
+    int cnt = 0;
+    for (int t = 0; t < ni; ++t) cnt += idle[t] / m == a;
+    if (!cnt) continue;
+    const int pick = s->head_rot[a] % cnt;
+    s->head_rot[a]++;
+    int seen = 0;
+    for (int t = 0; t < ni; ++t)
+      if (idle[t] / m == a && seen++ == pick) {
+        heads[nh++] = idle[t];
+        head_bits |= 1ull << idle[t];
+      }
+  }
+  shuffle(s, heads, nh);
+  chunk_into(&chunks, heads, nh, s->k);
+  for (int a = 0; a < s->nodes; ++a) {
+    int loc[RP_MAX_WORLD];
+    int nl = 0;
+    for (int t = 0; t < ni; ++t)
+      if (idle[t] / m == a && !((head_bits >> idle[t]) & 1)) loc[nl++] = idle[t];
+    shuffle(s, loc, nl);
+    chunk_into(&chunks, loc, nl, s->k);
+  }
+  for (int a = 0; a < s->nodes; ++a) {
+    std::vector<int> node;
+    for (int t = 0; t < ni; ++t)
+      if (idle[t] / m == a) node.push_back(idle[t]);
+    if (!node.empty()) chunks.push_back(node);
+  }
+  return push_groups(s, chunks);
 }
 
 int gg_request(GGState* s, int w, rp_group* out) {
@@ -258,7 +329,7 @@ int gg_done(GGState* s, int64_t seq, rp_group* released) {
     for (int q = 1; q < s->gb_len[m]; ++q) s->gb[m][q - 1] = s->gb[m][q];
     s->gb_len[m]--;
     s->handed[m] = -1;
-    s->lock &= ~(1ull << m);
+    if (s->gb_len[m] == 0) s->lock &= ~(1ull << m);
     if ((s->retiring >> m) & 1) {  // reading R19: retire atomically with the completion
       s->retiring &= ~(1ull << m);
       s->retired |= 1ull << m;

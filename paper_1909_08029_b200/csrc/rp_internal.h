@@ -48,6 +48,10 @@ struct GGState {
   GGGroup table[kTableCap];
   int64_t gd_calls, requests, max_depth;
   int64_t next_ticket;            // complete-arrival order of groups (shared GG)
+  // Inter-Intra Synchronization (§5.2): nodes > 0 splits every division into an
+  // Inter and an Intra round; head_rot[a] rotates node a's Head Worker
+  int32_t nodes;
+  int32_t head_rot[RP_MAX_WORLD];
   // random GG (§4.1)
   int32_t policy;
   int32_t npending;
@@ -57,7 +61,7 @@ struct GGState {
   int64_t n_pending, n_granted;
 };
 
-void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy = kPolicyGD);
+void gg_init(GGState* s, int n, int k, int c_thres, uint64_t seed, int policy = kPolicyGD, int nodes = 0);
 // Returns RP_OK and fills *out, RP_EAGAIN (random GG: the worker's group waits in the
 // pending queue; *out holds it; call again), or an RP_E* code.
 int gg_request(GGState* s, int w, rp_group* out);

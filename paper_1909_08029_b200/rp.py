@@ -27,6 +27,7 @@ RP_FLAG_TRACE = 0x1
 RP_FLAG_TIMING = 0x2
 RP_FLAG_SHARED_GG = 0x4
 RP_FLAG_RANDOM_GG = 0x8
+RP_FLAG_INTER_INTRA = 0x10
 RP_SCHED_PAPER4 = 1
 RP_SCHED_SHIFT_K = 2
 RP_WAIT_DEVICE = -1

@@ -21,15 +21,17 @@ from paper_1909_08029_b200.runner import LockstepRunner  # noqa: E402
 
 def main():
     # one JSON positional argument (torchrun would try to parse --options after the script)
-    a = argparse.Namespace(**{"rule": None, "steps": 10, "sample": 0, **json.loads(sys.argv[1])})
+    a = argparse.Namespace(**{"rule": None, "steps": 10, "sample": 0, "ii": False, **json.loads(sys.argv[1])})
     dist.init_process_group("gloo")
     rank, ngpu = dist.get_rank(), dist.get_world_size()
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local_rank)
     world = a.wpg * ngpu
-    nodes = ngpu if a.rule == "paper4" else 0
+    ii = bool(getattr(a, "ii", False))
+    nodes = ngpu if (a.rule == "paper4" or ii) else 0
+    import paper_1909_08029_b200 as rp
     r = LockstepRunner(world, a.n, mode=a.mode, rule=a.rule, group_size=a.k, n_gpus=ngpu, rank=rank,
-                       device=local_rank, nodes=nodes)
+                       device=local_rank, nodes=nodes, flags=rp.RP_FLAG_INTER_INTRA if ii else 0)
     log = r.run(a.steps)
     r.synchronize()
     slices = [(0, a.n)] if not a.sample else [(0, a.sample), (a.n // 2, a.n // 2 + a.sample),
@@ -37,7 +39,8 @@ def main():
     ok = True
     for lo, hi in slices:
         X, olog = sim.run_lockstep(world, a.n, a.steps, mode=a.mode, rule=a.rule, k=a.k, nodes=nodes,
-                                   m=(world // nodes if nodes else None), workers_per_gpu=a.wpg, lo=lo, hi=hi)
+                                   m=(world // nodes if nodes else None), workers_per_gpu=a.wpg, lo=lo, hi=hi,
+                                   ii_nodes=ngpu if ii else 0)
         for w in r.local:
             got = r.x(w)[lo:hi].cpu().numpy()
             if not np.array_equal(got.view(np.uint32), X[w].view(np.uint32)):

@@ -52,6 +52,8 @@ CASES = [
     (8, 1, 200_003, 3, "gd", None, 10, 0),                    # cfg 3 shape at 8 GPUs
     (8, 2, 100_003, 3, "static", "shift_k", 10, 0),           # cfg 4 shape at 8 GPUs
     (8, 8, 20_011, 3, "gd", None, 6, 0),                      # 64 workers: 8 cross parts per GPU
+    (2, 4, 50_007, 3, "gd+ii", None, 8, 0),                   # Inter-Intra (§5.2), GPU = node
+    (4, 8, 30_011, 3, "gd+ii", None, 8, 0),                   # configs[1] layout, Inter-Intra
 ]
 
 
@@ -59,7 +61,8 @@ CASES = [
 def test_multi_gpu_parity(gpus, wpg, n, k, mode, rule, steps, sample):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
-    _run(gpus, dict(wpg=wpg, n=n, k=k, mode=mode, rule=rule, steps=steps, sample=sample))
+    ii = mode == "gd+ii"
+    _run(gpus, dict(wpg=wpg, n=n, k=k, mode="gd" if ii else mode, rule=rule, steps=steps, sample=sample, ii=ii))
 
 
 ASYNC_CASES = [

@@ -106,3 +106,17 @@ def test_sixteen_workers_one_gpu_shift_k3():
     assert [g for _, g in log] == [sorted(gs) for _, gs in olog]
     _compare(r, X)
     r.close()
+
+
+def test_inter_intra_one_gpu():
+    # §5.2 on one node (GPU): Inter = a lone head + node-local groups of 3, Intra = all 8 workers
+    import paper_1909_08029_b200 as rp
+    n, T = 70_001, 10
+    r = LockstepRunner(8, n, mode="gd", group_size=3, nodes=1, flags=rp.RP_FLAG_INTER_INTRA)
+    log = r.run(T)
+    r.synchronize()
+    X, olog = sim.run_lockstep(8, n, T, mode="gd", k=3, ii_nodes=1)
+    assert [g for _, g in log] == [sorted(gs) for _, gs in olog]
+    assert olog[1][1] == [tuple(range(8))]               # the Intra step: one whole-node group
+    _compare(r, X)
+    r.close()

@@ -173,3 +173,56 @@ def test_random_gg_interleavings_bit_exact(n, k, seed, tmp_path):
     events = [json.loads(ln) for ln in open(trace)]
     from oracle import sim
     sim.replay_trace(events, n, 16, k=k, c_thres=0, seed_gd=seed, policy="random")
+
+
+@pytest.mark.parametrize("nodes,m,k,c_thres", [(4, 4, 3, 0), (2, 8, 3, 4), (8, 2, 2, 0), (1, 8, 3, 0), (3, 5, 4, 2)])
+def test_inter_intra_lockstep_bit_exact(nodes, m, k, c_thres):
+    n = nodes * m
+    og = GroupGenerator(n, k, c_thres=c_thres, seed_gd=9, nodes=nodes)
+    with rp.Context(n, 1024, n_gpus=0, group_size=k, c_thres=c_thres, seed_gd=9, nodes=nodes,
+                    flags=rp.RP_FLAG_INTER_INTRA) as c:
+        for _step in range(24):
+            seqs = set()
+            got = c.group_generate_many(list(range(n)))
+            for w in range(n):
+                seq, members = og.req(w)
+                assert (got[w].seq, tuple(got[w].member_list())) == (seq, members)
+                seqs.add(seq)
+            for s in sorted(seqs):
+                c.gg_release(s)
+                og.done(s)
+        assert c.stats()["max_gb_depth"] == 2
+
+
+def test_inter_intra_async_interleavings_bit_exact(tmp_path):
+    rnd = random.Random(5)
+    n, nodes, k = 12, 3, 3
+    og = GroupGenerator(n, k, c_thres=3, seed_gd=4, nodes=nodes)
+    left = [rnd.randint(2, 6) for _ in range(n)]
+    trace = tmp_path / "trace.jsonl"
+    with rp.Context(n, 1024, n_gpus=0, group_size=k, c_thres=3, seed_gd=4, nodes=nodes,
+                    flags=rp.RP_FLAG_INTER_INTRA) as c:
+        c.trace_open(trace)
+        while True:
+            s = og.s
+            choices = [("req", w) for w in range(n)
+                       if s.handed[w] == -1 and not (s.retired >> w) & 1 and (left[w] > 0 or s.gb[w])]
+            choices += [("done", q) for q, mem in s.groups.items() if all(s.handed[x] == q for x in mem)]
+            if not choices:
+                break
+            ev, a = rnd.choice(choices)
+            if ev == "req":
+                g = c.group_generate(a)
+                seq, mem = og.req(a)
+                assert (g.seq, tuple(g.member_list())) == (seq, mem)
+                if left[a] <= 1 and s.gb[a] == [seq]:
+                    c.retire(a)
+                    og.retire(a)
+            else:
+                c.gg_release(a)
+                for x in og.done(a):
+                    left[x] = max(0, left[x] - 1)
+        assert not any(left) and not og.s.groups
+    events = [json.loads(ln) for ln in open(trace)]
+    from oracle import sim
+    sim.replay_trace(events, n, 16, k=k, c_thres=3, seed_gd=4, ii_nodes=nodes)

@@ -15,6 +15,8 @@ def _clone(gg):
                   groups=dict(s.groups))
     c.trace = []
     c.gd_calls = gg.gd_calls
+    c.nodes = gg.nodes
+    c.head_rot = list(gg.head_rot)
     return c
 
 
@@ -108,35 +110,40 @@ def test_membership_frequency_uniform():
         assert abs(cnt[v] / trials - (k - 1) / (n - 1)) < 0.015
 
 
-def _explore(n, k, c_thres, iters, use_retire=True, seed=3):
+def _explore(n, k, c_thres, iters, use_retire=True, seed=3, nodes=0, depth_max=1):
     """DFS over every interleaving of request / completion events.
 
     Worker model (alg1 loop): compute -> request -> (all members requested) -> group
-    completes -> next iteration. Returns (states, deadlocks, max_gb_depth).
+    completes -> next iteration. A worker keeps requesting while it has iterations left or
+    groups queued in its GB (Inter-Intra queues two); it declares retirement (reading R19)
+    with the request that takes the last group it will ever run.
+    Returns (states, deadlocks, max_gb_depth).
     """
-    start = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed)
+    start = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed, nodes=nodes)
     stack = [(start, tuple([iters] * n))]
     seen = set()
     deadlocks = 0
     max_depth = 0
     while stack:
         gg, left = stack.pop()
-        key = (gg.s.key(), left)
+        key = (gg.s.key(), tuple(gg.head_rot), left)
         if key in seen:
             continue
         seen.add(key)
         s = gg.s
         max_depth = max(max_depth, gg.gb_depth())
-        # every worker is in at most one granted, unfinished group
-        held = Counter(w for m in s.groups.values() for w in m)
+        # groups at the head of all their members' GBs run concurrently: they must be disjoint
+        active = [m for q, m in s.groups.items() if all(s.gb[w] and s.gb[w][0] == q for w in m)]
+        held = Counter(w for m in active for w in m)
         assert all(c <= 1 for c in held.values())
         succ = []
         for w in range(n):
-            if left[w] > 0 and s.handed[w] == -1:
+            # Inter-Intra queues two groups: a worker serves what is queued for it before it stops
+            if s.handed[w] == -1 and not (s.retired >> w) & 1 and (left[w] > 0 or (nodes and s.gb[w])):
                 c = _clone(gg)
                 seq, g = c.req(w)                   # raises ConflictError on overlap
                 assert w in g                       # initiator is in its group (P:592)
-                if use_retire and left[w] == 1:
+                if use_retire and left[w] <= 1 and (not nodes or c.s.gb[w] == [seq]):
                     c.retire(w)
                 succ.append((c, left))
         for seq, members in s.groups.items():
@@ -145,7 +152,7 @@ def _explore(n, k, c_thres, iters, use_retire=True, seed=3):
                 c.done(seq)
                 nl = list(left)
                 for m in members:
-                    nl[m] -= 1
+                    nl[m] = max(0, nl[m] - 1)
                 succ.append((c, tuple(nl)))
         if not succ and (any(left) or s.groups):
             deadlocks += 1
@@ -181,3 +188,52 @@ def test_conflict_detection_is_live():
     gg.s.handed[0] = -1
     with pytest.raises(ConflictError):
         gg.req(0)
+
+
+def test_inter_intra_spec_example_2x2():
+    # S:360 (hand trace of §5.2 at minimum scale): 2 nodes x 2 workers, heads {0, 2}:
+    # Inter {0,2}, {1}, {3}; Intra {0,1}, {2,3}; every GB holds Inter then Intra.
+    gg = GroupGenerator(4, 2, c_thres=0, seed_gd=3, nodes=2)
+    seq, g = gg.req(0)
+    groups = [gg.s.groups[q] for q in sorted(gg.s.groups)]
+    assert sorted(groups[:3]) == [(0, 2), (1,), (3,)]
+    assert groups[3:] == [(0, 1), (2, 3)]
+    assert g == (0, 2)
+    assert all(len(b) == 2 for b in gg.s.gb)
+
+
+@pytest.mark.parametrize("nodes,m,k", [(4, 4, 3), (2, 8, 3), (8, 2, 2), (4, 4, 4)])
+def test_inter_intra_structure_lockstep(nodes, m, k):
+    # only Head Workers form cross-node groups, the rest is node-local; the
+    # Intra phase is one group per node; heads rotate; lockstep steps alternate Inter / Intra.
+    n = nodes * m
+    gg = GroupGenerator(n, k, c_thres=0, seed_gd=5, nodes=nodes)
+    heads_seen = [set() for _ in range(nodes)]
+    for step in range(2 * m):
+        seen = {}
+        for w in range(n):
+            seq, mem = gg.req(w)
+            seen[seq] = mem
+        groups = list(seen.values())
+        assert sorted(w for g in groups for w in g) == list(range(n))      # a partition
+        if step % 2 == 0:   # Inter
+            cross = [g for g in groups if len({w // m for w in g}) > 1]
+            for g in cross:
+                assert len({w // m for w in g}) == len(g)                   # <= 1 worker per node
+            for g in cross:
+                for w in g:
+                    heads_seen[w // m].add(w)
+        else:               # Intra: exactly the node partitions
+            assert sorted(groups) == [tuple(range(a * m, (a + 1) * m)) for a in range(nodes)]
+        for s in sorted(seen):
+            gg.done(s)
+    assert gg.head_rot == [m] * nodes        # one division per two steps; heads rotate per node
+    for a in range(nodes):
+        assert heads_seen[a] <= set(range(a * m, (a + 1) * m))
+    assert gg.gb_depth() == 0
+
+
+@pytest.mark.parametrize("n,nodes,k,iters", [(4, 2, 2, 1), (4, 2, 3, 1), (6, 2, 2, 1), (6, 3, 2, 1)])
+def test_inter_intra_brute_force(n, nodes, k, iters):
+    states, deadlocks, depth = _explore(n, k, 0, iters, nodes=nodes)
+    assert states > 10 and deadlocks == 0 and depth <= 2
