@@ -227,16 +227,24 @@ def run_ours(args, wl):
                     "algorithmic_bytes_per_launch": int(loc_b / max(1, sum(r["tim"]["local_launches"] for r in per_rank)))}
     nvl_roof = None
     if x_ms > 0:
-        a = x_b / (x_ms / 1e3) / 1e9        # per GPU: its NVLink read bytes / its kernel time
+        # the cross-GPU kernel moves NVLink bytes and (fused intra-GPU groups, pre-reduction)
+        # HBM bytes; its bound is whichever resource it uses the larger fraction of
+        a = x_b / (x_ms / 1e3) / 1e9        # per GPU: its NVLink bytes / its kernel time
+        xh = sum(r["tim"]["cross_bytes_hbm"] for r in per_rank)
+        ah = xh / (x_ms / 1e3) / 1e9
+        nl = sum(r["tim"]["cross_launches"] for r in per_rank)
         nvl_roof = {"bound": "nvlink", "kernel": "xgpu_kernel (fused SGD + P-Reduce, cross-GPU part)",
                     "achieved": round(a, 1), "peak": NVLINK_PEAK,
                     "peak_source": "fallback (B200_PROFILING.md: measured peer copy per direction; 900 nominal)",
                     "unit": "GB/s", "frac": round(a / NVLINK_PEAK, 4), "frac_of_nominal": round(a / NVLINK_NOMINAL, 4),
-                    "traffic": None,
-                    "launches": sum(r["tim"]["cross_launches"] for r in per_rank),
-                    "kernel_ms_per_launch": round(x_ms / max(1, sum(r["tim"]["cross_launches"] for r in per_rank)), 4),
-                    "algorithmic_nvlink_bytes_per_launch_per_gpu":
-                        int(x_b / max(1, sum(r["tim"]["cross_launches"] for r in per_rank)))}
+                    "traffic": None, "launches": nl,
+                    "kernel_ms_per_launch": round(x_ms / max(1, nl), 4),
+                    "algorithmic_nvlink_bytes_per_launch_per_gpu": int(x_b / max(1, nl)),
+                    "hbm_achieved": round(ah, 1), "hbm_frac": round(ah / peaks["hbm_gbs"], 4)}
+        if ah / peaks["hbm_gbs"] > a / NVLINK_PEAK:      # fused local work dominates: HBM-bound
+            nvl_roof.update({"bound": "hbm", "achieved": round(ah, 1), "peak": peaks["hbm_gbs"],
+                             "peak_source": peak_src, "frac": round(ah / peaks["hbm_gbs"], 4),
+                             "nvlink_achieved": round(a, 1), "nvlink_frac": round(a / NVLINK_PEAK, 4)})
     # the dominant kernel is the one with the larger share of device time
     main_is_nvl = bool(nvl_roof) and x_ms >= loc_ms
     roof = nvl_roof if main_is_nvl else (hbm_roof or nvl_roof)

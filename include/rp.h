@@ -139,6 +139,7 @@ typedef struct rp_timing {
   int64_t cross_launches;
   double cross_ms;
   int64_t cross_bytes_nvlink;
+  int64_t cross_bytes_hbm;    /* local HBM bytes of the cross launches (incl. fused groups) */
 } rp_timing;
 
 typedef struct rp_ctx rp_ctx;

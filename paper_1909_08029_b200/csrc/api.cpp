@@ -1132,6 +1132,7 @@ int rp_timing_read(rp_ctx* c, rp_timing* out) {
       r.cross_launches++;
       r.cross_ms += ms;
       r.cross_bytes_nvlink += t.bytes_nvlink;
+      r.cross_bytes_hbm += t.bytes_hbm;
     } else {
       r.local_launches++;
       r.local_ms += ms;

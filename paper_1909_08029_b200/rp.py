@@ -96,7 +96,8 @@ class rp_timing(ctypes.Structure):
                 ("max_ms", ctypes.c_double), ("bytes_hbm", ctypes.c_int64), ("bytes_nvlink", ctypes.c_int64),
                 ("local_launches", ctypes.c_int64), ("local_ms", ctypes.c_double),
                 ("local_bytes_hbm", ctypes.c_int64), ("cross_launches", ctypes.c_int64),
-                ("cross_ms", ctypes.c_double), ("cross_bytes_nvlink", ctypes.c_int64)]
+                ("cross_ms", ctypes.c_double), ("cross_bytes_nvlink", ctypes.c_int64),
+                ("cross_bytes_hbm", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
