@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "rp_internal.h"
@@ -148,10 +149,13 @@ __device__ __forceinline__ void loop_if(const MultiTask& t, int gi, int first, i
   if constexpr (K <= KMAX) group_loop<K, U>(t, gi, first, n4, n);
 }
 
-// KMAX bounds the instantiated group sizes (and so the register budget).
-template <int KMAX, int U>
-__global__ void __launch_bounds__(kThreads) preduce_multi_kernel(const MultiTask t, const int64_t n4,
-                                                                const int64_t n) {
+// KMAX bounds the instantiated group sizes (and so the register budget); MINB is the
+// resident-CTA floor given to ptxas (RP_PREDUCE_MINB selects 2 for k <= 4, 3 or 4 for
+// k <= 8: more warps in flight vs all 2k loads of a thread in registers;
+// profiles/r01_hbm_probe_k8.txt).
+template <int KMAX, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) preduce_multi_kernel(const MultiTask t, const int64_t n4,
+                                                                      const int64_t n) {
   int gi = 0;
   while (gi + 1 < t.ngroups && static_cast<int>(blockIdx.x) >= t.cta_begin[gi + 1]) ++gi;
   const int first = t.group_first[gi];
@@ -177,11 +181,11 @@ __global__ void __launch_bounds__(kThreads) preduce_multi_kernel(const MultiTask
 
 int g_num_sms = 0;
 
-template <int KMAX, int U>
+template <int KMAX, int U, int MINB>
 int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
   static int occ = 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<KMAX, U>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<KMAX, U, MINB>, kThreads, 0) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
@@ -206,7 +210,7 @@ int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     acc += static_cast<int32_t>(share);
   }
   t.cta_begin[t.ngroups] = acc;
-  preduce_multi_kernel<KMAX, U><<<acc, kThreads, 0, stream>>>(t, n4, n);
+  preduce_multi_kernel<KMAX, U, MINB><<<acc, kThreads, 0, stream>>>(t, n4, n);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("preduce kernel launch: ") + cudaGetErrorString(e);
@@ -239,10 +243,19 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     }
   }
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (kmax <= 2) return launch_kmax<2, 2>(t, n, s, err);
-  if (kmax <= 4) return launch_kmax<4, 2>(t, n, s, err);
-  if (kmax <= 8) return launch_kmax<8, 1>(t, n, s, err);
-  return launch_kmax<16, 1>(t, n, s, err);
+  static int minb = -1;  // RP_PREDUCE_MINB: resident-CTA floor for the k <= 4 and k <= 8 kernels
+  if (minb < 0) {
+    const char* v = std::getenv("RP_PREDUCE_MINB");
+    minb = v && *v ? std::atoi(v) : 0;
+  }
+  if (kmax <= 2) return launch_kmax<2, 2, 1>(t, n, s, err);
+  if (kmax <= 4) return minb == 2 ? launch_kmax<4, 2, 2>(t, n, s, err) : launch_kmax<4, 2, 1>(t, n, s, err);
+  if (kmax <= 8) {
+    if (minb == 3) return launch_kmax<8, 1, 3>(t, n, s, err);
+    if (minb == 4) return launch_kmax<8, 1, 4>(t, n, s, err);
+    return launch_kmax<8, 1, 1>(t, n, s, err);
+  }
+  return launch_kmax<16, 1, 1>(t, n, s, err);
 }
 
 }  // namespace rp
