@@ -257,6 +257,15 @@ int rp_retire(rp_ctx* ctx, int32_t w);
  * RP_EINVAL (misaligned / no buffer). */
 int rp_step(rp_ctx* ctx, int32_t w, const float* grad_dev, float lr);
 
+/* rp_step with the paper's ResNet-50 optimizer ("Momentum optimizer is
+ * used with momentum=0.9 and weight_decay=1e-4"; reading R24): inside the fused
+ * kernel, per element, g' = fl(g + fl(wd*x)); v <- fl(fl(momentum*v) + g');
+ * y = fl(x - fl(lr*v)). v_dev is the worker's momentum buffer (n_params fp32,
+ * 16-byte aligned device memory, borrowed, zero-initialized by the caller); it
+ * stays per worker (only the weights are averaged). Errors as rp_step. */
+int rp_step_momentum(rp_ctx* ctx, int32_t w, const float* grad_dev, float lr, float momentum,
+                     float weight_decay, float* v_dev);
+
 /* Collective arrival of worker w at group g (alg1 step 4). Every
  * member must call with an identical group. The last local
  * arriver enqueues the fused kernel on its worker stream after the other

@@ -34,11 +34,16 @@ def init_replicas(n, n_params, lo=0, hi=None):
 
 def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
                  rule=None, k=None, nodes=None, m=None, c_thres=4, seed_gd=3,
-                 lo=0, hi=None, X=None, first_step=1, gg=None, log=None, ii_nodes=0):
+                 lo=0, hi=None, X=None, first_step=1, gg=None, log=None, ii_nodes=0,
+                 section_length=1, momentum=None, V=None):
     """Simulate `steps` lockstep steps; returns (X, log).
 
     mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter; ii_nodes > 0
     makes every division Inter-Intra, §5.2).
+    section_length L ("# of iterations between two synchronizations"): only steps
+    t with t % L == 0 synchronize; the others are SGD only (no group requested).
+    momentum = (mu, wd): alg1 step 2 with momentum + weight decay; per-worker
+    momentum buffers V (zero-initialized) stay local.
     [lo, hi) restricts the simulated element range (elementwise method, so a
     slice is computed exactly as in the full run).
     log: list receiving (t, [groups]) per step, groups as sorted tuples.
@@ -49,8 +54,13 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
     log = [] if log is None else log
     if mode == "gd" and gg is None:
         gg = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed_gd, nodes=ii_nodes)
+    if momentum is not None and V is None:
+        V = {w: np.zeros(hi - lo, F32) for w in range(n)}
+    mu, wd = momentum if momentum is not None else (0.0, 0.0)
     for t in range(first_step, first_step + steps):
-        if mode == "static":
+        if section_length > 1 and t % section_length != 0:
+            groups = []
+        elif mode == "static":
             groups = [tuple(g) for g in sched_mod.groups_for(rule, t, n=n, k=k, nodes=nodes, m=m)]
         elif mode == "gd":
             seen = {}
@@ -65,10 +75,10 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
         in_group = set(w for g in groups for w in g)
         for g in groups:
             G = {w: xi_mod.grad(w, t, n_params, lo, hi) for w in g}
-            fused_group_update(X, G, g, lr, wpg)
+            fused_group_update(X, G, g, lr, wpg, V=V, mu=mu, wd=wd)
         for w in range(n):
             if w not in in_group:           # skip: SGD only (singleton)
-                fused_group_update(X, {w: xi_mod.grad(w, t, n_params, lo, hi)}, (w,), lr, wpg)
+                fused_group_update(X, {w: xi_mod.grad(w, t, n_params, lo, hi)}, (w,), lr, wpg, V=V, mu=mu, wd=wd)
         log.append((t, [tuple(g) for g in groups] + [(w,) for w in range(n) if w not in in_group]))
     return X, log
 

@@ -35,6 +35,17 @@ def sgd_fp32(x, g, lr):
     return x - prod                             # one rounding
 
 
+def momentum_sgd_fp32(x, g, v, lr, mu, wd):
+    """alg1 step 2 with the paper's ResNet-50 optimizer ("Momentum optimizer is used with
+    momentum=0.9 and weight_decay=1e-4"; TF MomentumOptimizer with an L2 term, reading R24):
+        g' = fl(g + fl(wd*x));  v <- fl(fl(mu*v) + g');  y = fl(x - fl(lr*v)).
+    Returns (y, v_new); each line is one fp32 rounding."""
+    x = np.asarray(x, dtype=F32)
+    gp = np.asarray(g, dtype=F32) + F32(wd) * x
+    v_new = F32(mu) * np.asarray(v, dtype=F32) + gp
+    return x - F32(lr) * v_new, v_new
+
+
 def _fold_order(members, workers_per_gpu):
     """Members grouped by GPU in ascending GPU id, each list ascending (reading R1/R6)."""
     by_gpu = {}
@@ -59,14 +70,20 @@ def preduce_fp32(ys, members, workers_per_gpu=None):
     return s / F32(len(members))
 
 
-def fused_group_update(X, G, members, lr, workers_per_gpu=None):
+def fused_group_update(X, G, members, lr, workers_per_gpu=None, V=None, mu=0.0, wd=0.0):
     """Apply alg1 steps 2+4 for one group in place on X (dict or list of fp32 vectors).
 
     G: dict member -> gradient vector or None (no staged step).
+    V: optional dict member -> momentum buffer (updated in place) for momentum_sgd_fp32.
     Returns the mean written to every member ("x_g <- xbar_G").
     """
     members = sorted(members)
-    ys = {m: sgd_fp32(X[m], G.get(m), lr) for m in members}
+    ys = {}
+    for m in members:
+        if V is not None and m in V and G.get(m) is not None:
+            ys[m], V[m] = momentum_sgd_fp32(X[m], G[m], V[m], lr, mu, wd)
+        else:
+            ys[m] = sgd_fp32(X[m], G.get(m), lr)
     if len(members) == 1:
         # |G| = 1: fl(y / 1) = y exactly; F^G is the identity (SURVEY c.3 "singleton = SGD only").
         X[members[0]] = ys[members[0]]

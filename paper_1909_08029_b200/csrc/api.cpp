@@ -63,8 +63,7 @@ struct WorkerSlot {
   cudaEvent_t ev_group = nullptr;   // completion of a group this worker launched
   cudaEvent_t ev_done = nullptr;    // this worker's group is done, in its stream order
   bool staged = false;
-  const float* grad = nullptr;
-  float lr = 0.f;
+  rp::MemberUpdate upd{};  // the staged alg1 step 2
   bool in_group = false;  // arrived at a group and not yet waited
   int64_t seq = 0;
 };
@@ -77,8 +76,7 @@ struct ActiveGroup {
   uint64_t waited = 0;
   bool launched = false;
   bool released = false;  // GG release done (first observed completion)
-  const float* grad[RP_MAX_GROUP] = {};
-  float lr[RP_MAX_GROUP] = {};
+  rp::MemberUpdate u[RP_MAX_GROUP] = {};  // alg1 step 2 of each member (staged by rp_step*)
 };
 
 std::string members_str(const rp_group& g, uint64_t mask_filter = ~0ull) {
@@ -93,6 +91,13 @@ std::string members_str(const rp_group& g, uint64_t mask_filter = ~0ull) {
   }
   os << "]";
   return os.str();
+}
+
+// Algorithmic HBM bytes per element of one member: x read + x write, g read if stepped,
+// v read + write with momentum.
+int64_t member_bytes(const rp::MemberUpdate& u) {
+  if (!u.g) return 8;
+  return u.v ? 20 : 12;
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -283,9 +288,8 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
       t.group_first[t.ngroups] = nm;
       for (int i = 0; i < a.g.size; ++i) {
         t.x[nm] = c->w[a.g.members[i]].x;
-        t.g[nm] = a.grad[i];
-        t.lr[nm] = a.lr[i];
-        bytes += (a.grad[i] ? 12 : 8) * c->cfg.n_params;
+        t.u[nm] = a.u[i];
+        bytes += member_bytes(a.u[i]) * c->cfg.n_params;
         ++nm;
       }
       t.ngroups++;
@@ -372,8 +376,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
       if (gpu == c->cfg.rank) {
         if (p.m >= rp::kMaxXLocal) return fail(RP_EINVAL, "more than 8 local members in a cross-GPU group");
         p.x[p.m] = c->w[m].x;
-        p.g[p.m] = a.grad[i];
-        p.lr[p.m] = a.lr[i];
+        p.u[p.m] = a.u[i];
         p.m++;
       }
     }
@@ -388,9 +391,8 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
     G.k = a.g.size;
     for (int i = 0; i < a.g.size; ++i) {
       G.x[i] = c->w[a.g.members[i]].x;
-      G.g[i] = a.grad[i];
-      G.lr[i] = a.lr[i];
-      hbm_local += (a.grad[i] ? 12 : 8) * T.n;
+      G.u[i] = a.u[i];
+      hbm_local += member_bytes(a.u[i]) * T.n;
     }
     c->stats.groups_launched++;
     if (a.g.size == 1) c->stats.singleton_groups++;
@@ -432,7 +434,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
     const int64_t others = T.n - mine;
     nvl += 4 * (others + (p.kp - 1) * mine);
     int64_t rd = 0;
-    for (int m = 0; m < p.m; ++m) rd += p.g[m] ? 8 : 4;
+    for (int m = 0; m < p.m; ++m) rd += member_bytes(p.u[m]) - 4;  // reads (x, g, v) + v write
     // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
     hbm += rd * T.n + 4 * (p.kp - 1) * mine + 4 * p.m * mine + 8 * (p.m - 1) * others;
   }
@@ -954,8 +956,22 @@ int rp_step(rp_ctx* c, int32_t w, const float* grad, float lr) {
   if (!gp) return fail(RP_EINVAL, "rp_step: no gradient buffer");
   if (reinterpret_cast<uintptr_t>(gp) & 15) return fail(RP_EINVAL, "rp_step: gradient must be 16-byte aligned");
   s.staged = true;
-  s.grad = gp;
-  s.lr = lr;
+  s.upd = rp::MemberUpdate{gp, nullptr, lr, 0.f, 0.f};
+  return RP_OK;
+}
+
+int rp_step_momentum(rp_ctx* c, int32_t w, const float* grad, float lr, float momentum, float weight_decay,
+                     float* v_dev) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!v_dev || (reinterpret_cast<uintptr_t>(v_dev) & 15))
+    return fail(RP_EINVAL, "rp_step_momentum: momentum buffer must be a non-null 16-byte aligned device pointer");
+  const int rc = rp_step(c, w, grad, lr);
+  if (rc != RP_OK) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  WorkerSlot& s = c->w[w];
+  s.upd.v = v_dev;
+  s.upd.mu = momentum;
+  s.upd.wd = weight_decay;
   return RP_OK;
 }
 
@@ -1007,8 +1023,7 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
                            "or be a shared-GG group (RP_FLAG_SHARED_GG)");
   int idx = 0;
   while (g->members[idx] != w) ++idx;
-  a.grad[idx] = s.staged ? s.grad : nullptr;
-  a.lr[idx] = s.staged ? s.lr : 0.f;
+  a.u[idx] = s.staged ? s.upd : rp::MemberUpdate{};
   CUDA_TRY(cudaEventRecord(s.ev_arrive, s.stream));
   s.staged = false;
   s.in_group = true;

@@ -26,6 +26,7 @@
 #include <string>
 
 #include "rp_internal.h"
+#include "update.cuh"
 
 namespace rp {
 
@@ -54,9 +55,6 @@ __device__ __forceinline__ void st_x(float* p, float4 v) {
                : "memory");
 }
 
-// y = fl(x - fl(lr*g))
-__device__ __forceinline__ float sgd(float x, float g, float lr) { return __fsub_rn(x, __fmul_rn(lr, g)); }
-
 template <int K>
 __device__ __forceinline__ float fold_mean(const float (&y)[K]) {
   float s = y[0];
@@ -65,19 +63,24 @@ __device__ __forceinline__ float fold_mean(const float (&y)[K]) {
   return K == 1 ? s : __fdiv_rn(s, static_cast<float>(K));
 }
 
-// One tile of the group whose members start at `first`: float4 indices [i0, i0 + kThreads*U) of every member.
-template <int K, int U>
+__device__ __forceinline__ float4 ld_v(const float* p) {
+  float4 v;
+  asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+
+// One tile of the group whose members start at `first`: float4 indices [i0, i0 + kThreads*U)
+// of every member. MOM: some member carries a momentum buffer (read and written here).
+template <int K, int U, bool MOM>
 __device__ __forceinline__ void group_tile(const MultiTask& t, int first, int64_t i0, int64_t n4) {
   float* x[K];
-  const float* g[K];
-  float lr[K];
+  MemberUpdate up[K];
 #pragma unroll
   for (int m = 0; m < K; ++m) {
     x[m] = t.x[first + m];
-    g[m] = t.g[first + m];
-    lr[m] = t.lr[first + m];
+    up[m] = t.u[first + m];
   }
-  float4 xv[U][K], gv[U][K];
+  float4 xv[U][K], gv[U][K], vv[U][MOM ? K : 1];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t i = i0 + static_cast<int64_t>(u) * kThreads + threadIdx.x;
@@ -85,7 +88,9 @@ __device__ __forceinline__ void group_tile(const MultiTask& t, int first, int64_
 #pragma unroll
       for (int m = 0; m < K; ++m) {
         xv[u][m] = ld_x(x[m] + 4 * i);
-        if (g[m] != nullptr) gv[u][m] = ld_g(g[m] + 4 * i);
+        if (up[m].g != nullptr) gv[u][m] = ld_g(up[m].g + 4 * i);
+        if constexpr (MOM)
+          if (up[m].v != nullptr) vv[u][m] = ld_v(up[m].v + 4 * i);
       }
     }
   }
@@ -96,17 +101,14 @@ __device__ __forceinline__ void group_tile(const MultiTask& t, int first, int64_
       float yx[K], yy[K], yz[K], yw[K];
 #pragma unroll
       for (int m = 0; m < K; ++m) {
-        if (g[m] != nullptr) {
-          yx[m] = sgd(xv[u][m].x, gv[u][m].x, lr[m]);
-          yy[m] = sgd(xv[u][m].y, gv[u][m].y, lr[m]);
-          yz[m] = sgd(xv[u][m].z, gv[u][m].z, lr[m]);
-          yw[m] = sgd(xv[u][m].w, gv[u][m].w, lr[m]);
-        } else {
-          yx[m] = xv[u][m].x;
-          yy[m] = xv[u][m].y;
-          yz[m] = xv[u][m].z;
-          yw[m] = xv[u][m].w;
-        }
+        float4 vm = MOM ? vv[u][MOM ? m : 0] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 y = step4<MOM>(xv[u][m], gv[u][m], vm, up[m]);
+        if constexpr (MOM)
+          if (up[m].v != nullptr && up[m].g != nullptr) st_x(up[m].v + 4 * i, vm);
+        yx[m] = y.x;
+        yy[m] = y.y;
+        yz[m] = y.z;
+        yw[m] = y.w;
       }
       const float4 r = make_float4(fold_mean<K>(yx), fold_mean<K>(yy), fold_mean<K>(yz), fold_mean<K>(yw));
 #pragma unroll
@@ -116,15 +118,11 @@ __device__ __forceinline__ void group_tile(const MultiTask& t, int first, int64_
 }
 
 // Element j of the group whose members start at `first`, scalar (the n mod 4 tail).
-template <int K>
+template <int K, bool MOM>
 __device__ __forceinline__ void group_scalar(const MultiTask& t, int first, int64_t j) {
   float y[K];
 #pragma unroll
-  for (int m = 0; m < K; ++m) {
-    const float* g = t.g[first + m];
-    const float xj = t.x[first + m][j];
-    y[m] = g != nullptr ? sgd(xj, g[j], t.lr[first + m]) : xj;
-  }
+  for (int m = 0; m < K; ++m) y[m] = step1<MOM>(t.x[first + m][j], t.u[first + m], j);
   const float r = fold_mean<K>(y);
 #pragma unroll
   for (int m = 0; m < K; ++m) t.x[first + m][j] = r;
@@ -134,58 +132,58 @@ __device__ __forceinline__ void group_scalar(const MultiTask& t, int first, int6
 // shared out in proportion to each group's bytes), so a CTA runs a single
 // K-specialized loop for its whole life. Each CTA grid-strides over its group's
 // tiles.
-template <int K, int U>
+template <int K, int U, bool MOM>
 __device__ __forceinline__ void group_loop(const MultiTask& t, int gi, int first, int64_t n4, int64_t n) {
   const int64_t nb = t.cta_begin[gi + 1] - t.cta_begin[gi];
   const int64_t b = static_cast<int64_t>(blockIdx.x) - t.cta_begin[gi];
   const int64_t tiles = (n4 + kThreads * U - 1) / (kThreads * U);
-  for (int64_t tile = b; tile < tiles; tile += nb) group_tile<K, U>(t, first, tile * kThreads * U, n4);
+  for (int64_t tile = b; tile < tiles; tile += nb) group_tile<K, U, MOM>(t, first, tile * kThreads * U, n4);
   const int64_t rem = n - 4 * n4;  // ragged tail: first CTA of the group, scalar
-  if (b == 0 && threadIdx.x < rem) group_scalar<K>(t, first, 4 * n4 + threadIdx.x);
+  if (b == 0 && threadIdx.x < rem) group_scalar<K, MOM>(t, first, 4 * n4 + threadIdx.x);
 }
 
-template <int K, int U, int KMAX>
+template <int K, int U, int KMAX, bool MOM>
 __device__ __forceinline__ void loop_if(const MultiTask& t, int gi, int first, int64_t n4, int64_t n) {
-  if constexpr (K <= KMAX) group_loop<K, U>(t, gi, first, n4, n);
+  if constexpr (K <= KMAX) group_loop<K, U, MOM>(t, gi, first, n4, n);
 }
 
 // KMAX bounds the instantiated group sizes (and so the register budget); MINB is the
 // resident-CTA floor given to ptxas (RP_PREDUCE_MINB selects 2 for k <= 4, 3 or 4 for
 // k <= 8: more warps in flight vs all 2k loads of a thread in registers;
 // profiles/r01_hbm_probe_k8.txt).
-template <int KMAX, int U, int MINB>
+template <int KMAX, int U, int MINB, bool MOM>
 __global__ void __launch_bounds__(kThreads, MINB) preduce_multi_kernel(const MultiTask t, const int64_t n4,
                                                                       const int64_t n) {
   int gi = 0;
   while (gi + 1 < t.ngroups && static_cast<int>(blockIdx.x) >= t.cta_begin[gi + 1]) ++gi;
   const int first = t.group_first[gi];
   switch (t.group_k[gi]) {
-    case 1: loop_if<1, U, KMAX>(t, gi, first, n4, n); break;
-    case 2: loop_if<2, U, KMAX>(t, gi, first, n4, n); break;
-    case 3: loop_if<3, U, KMAX>(t, gi, first, n4, n); break;
-    case 4: loop_if<4, U, KMAX>(t, gi, first, n4, n); break;
-    case 5: loop_if<5, U, KMAX>(t, gi, first, n4, n); break;
-    case 6: loop_if<6, U, KMAX>(t, gi, first, n4, n); break;
-    case 7: loop_if<7, U, KMAX>(t, gi, first, n4, n); break;
-    case 8: loop_if<8, U, KMAX>(t, gi, first, n4, n); break;
-    case 9: loop_if<9, U, KMAX>(t, gi, first, n4, n); break;
-    case 10: loop_if<10, U, KMAX>(t, gi, first, n4, n); break;
-    case 11: loop_if<11, U, KMAX>(t, gi, first, n4, n); break;
-    case 12: loop_if<12, U, KMAX>(t, gi, first, n4, n); break;
-    case 13: loop_if<13, U, KMAX>(t, gi, first, n4, n); break;
-    case 14: loop_if<14, U, KMAX>(t, gi, first, n4, n); break;
-    case 15: loop_if<15, U, KMAX>(t, gi, first, n4, n); break;
-    default: loop_if<16, U, KMAX>(t, gi, first, n4, n); break;
+    case 1: loop_if<1, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 2: loop_if<2, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 3: loop_if<3, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 4: loop_if<4, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 5: loop_if<5, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 6: loop_if<6, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 7: loop_if<7, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 8: loop_if<8, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 9: loop_if<9, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 10: loop_if<10, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 11: loop_if<11, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 12: loop_if<12, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 13: loop_if<13, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 14: loop_if<14, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    case 15: loop_if<15, U, KMAX, MOM>(t, gi, first, n4, n); break;
+    default: loop_if<16, U, KMAX, MOM>(t, gi, first, n4, n); break;
   }
 }
 
 int g_num_sms = 0;
 
-template <int KMAX, int U, int MINB>
+template <int KMAX, int U, int MINB, bool MOM>
 int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
   static int occ = 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<KMAX, U, MINB>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, preduce_multi_kernel<KMAX, U, MINB, MOM>, kThreads, 0) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
@@ -210,7 +208,7 @@ int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     acc += static_cast<int32_t>(share);
   }
   t.cta_begin[t.ngroups] = acc;
-  preduce_multi_kernel<KMAX, U, MINB><<<acc, kThreads, 0, stream>>>(t, n4, n);
+  preduce_multi_kernel<KMAX, U, MINB, MOM><<<acc, kThreads, 0, stream>>>(t, n4, n);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("preduce kernel launch: ") + cudaGetErrorString(e);
@@ -237,7 +235,8 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     kmax = std::max(kmax, k);
   }
   for (int i = 0; i < nm; ++i) {
-    if (!t.x[i] || (reinterpret_cast<uintptr_t>(t.x[i]) & 15) || (reinterpret_cast<uintptr_t>(t.g[i]) & 15)) {
+    if (!t.x[i] || (reinterpret_cast<uintptr_t>(t.x[i]) & 15) || (reinterpret_cast<uintptr_t>(t.u[i].g) & 15) ||
+        (reinterpret_cast<uintptr_t>(t.u[i].v) & 15)) {
       *err = "preduce: replica and gradient pointers must be non-null and 16-byte aligned";
       return RP_EINVAL;
     }
@@ -248,14 +247,23 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     const char* v = std::getenv("RP_PREDUCE_MINB");
     minb = v && *v ? std::atoi(v) : 0;
   }
-  if (kmax <= 2) return launch_kmax<2, 2, 1>(t, n, s, err);
-  if (kmax <= 4) return minb == 2 ? launch_kmax<4, 2, 2>(t, n, s, err) : launch_kmax<4, 2, 1>(t, n, s, err);
-  if (kmax <= 8) {
-    if (minb == 3) return launch_kmax<8, 1, 3>(t, n, s, err);
-    if (minb == 4) return launch_kmax<8, 1, 4>(t, n, s, err);
-    return launch_kmax<8, 1, 1>(t, n, s, err);
+  bool mom = false;
+  for (int i = 0; i < nm; ++i) mom = mom || (t.u[i].v != nullptr && t.u[i].g != nullptr);
+  if (mom) {  // momentum buffers: a separate instantiation keeps the plain path's registers
+    if (kmax <= 2) return launch_kmax<2, 2, 1, true>(t, n, s, err);
+    if (kmax <= 4) return launch_kmax<4, 1, 1, true>(t, n, s, err);
+    if (kmax <= 8) return launch_kmax<8, 1, 1, true>(t, n, s, err);
+    return launch_kmax<16, 1, 1, true>(t, n, s, err);
   }
-  return launch_kmax<16, 1, 1>(t, n, s, err);
+  if (kmax <= 2) return launch_kmax<2, 2, 1, false>(t, n, s, err);
+  if (kmax <= 4)
+    return minb == 2 ? launch_kmax<4, 2, 2, false>(t, n, s, err) : launch_kmax<4, 2, 1, false>(t, n, s, err);
+  if (kmax <= 8) {
+    if (minb == 3) return launch_kmax<8, 1, 3, false>(t, n, s, err);
+    if (minb == 4) return launch_kmax<8, 1, 4, false>(t, n, s, err);
+    return launch_kmax<8, 1, 1, false>(t, n, s, err);
+  }
+  return launch_kmax<16, 1, 1, false>(t, n, s, err);
 }
 
 }  // namespace rp

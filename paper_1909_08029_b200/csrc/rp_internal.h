@@ -71,6 +71,15 @@ int gg_retire(GGState* s, int w);
 const GGGroup* gg_find(const GGState* s, int64_t seq);
 
 // ---- kernels (preduce.cu, xi.cu) -------------------------------------------------------
+// alg1 step 2 for one member, applied inside the fused kernels:
+//   plain SGD:             y = fl(x - fl(lr g))
+//   momentum + L2: g' = fl(g + fl(wd x)); v = fl(fl(mu v) + g'); y = fl(x - fl(lr v))
+//   no staged step (g = nullptr): y = x
+struct MemberUpdate {
+  const float* g;  // gradient, or nullptr
+  float* v;        // momentum buffer (read-modify-write), or nullptr for plain SGD
+  float lr, mu, wd;
+};
 // Several disjoint groups executed by one launch: members of group gi are
 // entries group_first[gi] .. group_first[gi] + group_k[gi] - 1 (packed, in
 // ascending worker id). cta_begin is filled by the launcher.
@@ -81,8 +90,7 @@ struct MultiTask {
   int32_t group_k[kMaxTasks];
   int32_t group_first[kMaxTasks];
   float* x[kMaxTaskMembers];
-  const float* g[kMaxTaskMembers];   // nullptr: member has no staged step (y = x)
-  float lr[kMaxTaskMembers];
+  MemberUpdate u[kMaxTaskMembers];
   int32_t cta_begin[kMaxTasks + 1];
 };
 
@@ -110,8 +118,7 @@ struct XPart {
   uint64_t tag;       // nonzero, unique per group
   int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry)
   float* x[kMaxXLocal];
-  const float* g[kMaxXLocal];
-  float lr[kMaxXLocal];
+  MemberUpdate u[kMaxXLocal];
   float* xfirst[kMaxXGpus];               // first local member replica of each group GPU (mapped)
   float* stage[kMaxXGpus];                // staging region of each group GPU for this group (mapped)
   unsigned long long* pflags[kMaxXGpus];  // flag array of each group GPU (mapped or local)
@@ -131,8 +138,7 @@ constexpr int kMaxFusedK = 4;
 struct XLocalGroup {
   int32_t k;
   float* x[kMaxFusedK];
-  const float* g[kMaxFusedK];
-  float lr[kMaxFusedK];
+  MemberUpdate u[kMaxFusedK];
 };
 
 // Kernel parameters exceed 4 KB: CUDA >= 12.1 large-parameter launches (sm_70+).

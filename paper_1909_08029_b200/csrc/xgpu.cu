@@ -46,6 +46,7 @@
 #include <vector>
 
 #include "rp_internal.h"
+#include "update.cuh"
 
 namespace rp {
 
@@ -81,10 +82,6 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ float sgd1(float x, float g, float lr) { return __fsub_rn(x, __fmul_rn(lr, g)); }
-__device__ __forceinline__ float4 sgd4(float4 x, float4 g, float lr) {
-  return make_float4(sgd1(x.x, g.x, lr), sgd1(x.y, g.y, lr), sgd1(x.z, g.z, lr), sgd1(x.w, g.w, lr));
-}
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
@@ -103,29 +100,40 @@ __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned 
   while (ld_acquire_sys(f) != tag) __nanosleep(32);
 }
 
-// Local partial of my p.m (<= M) members at float4 index i (left fold, ascending worker id).
-template <int M>
+// Local partial of my p.m (<= M) members at float4 index i (left fold, ascending worker id),
+// with alg1 step 2 applied (and momentum buffers updated: each element's partial is
+// computed exactly once, in its A or B item).
+template <int M, bool MOM>
 __device__ __forceinline__ float4 local_partial4(const XPart& p, int64_t i) {
-  float4 xv[M], gv[M];
+  float4 xv[M], gv[M], vv[MOM ? M : 1];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     if (m < p.m) {
       xv[m] = ldv(p.x[m] + 4 * i);
-      if (p.g[m]) gv[m] = ldg_nc(p.g[m] + 4 * i);
+      if (p.u[m].g) gv[m] = ldg_nc(p.u[m].g + 4 * i);
+      if constexpr (MOM)
+        if (p.u[m].v) vv[m] = ldv(p.u[m].v + 4 * i);
     }
   }
-  float4 s = p.g[0] ? sgd4(xv[0], gv[0], p.lr[0]) : xv[0];
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int m = 1; m < M; ++m)
-    if (m < p.m) s = add4(s, p.g[m] ? sgd4(xv[m], gv[m], p.lr[m]) : xv[m]);
+  for (int m = 0; m < M; ++m) {
+    if (m < p.m) {
+      float4 vm = vv[MOM ? m : 0];
+      const float4 y = step4<MOM>(xv[m], gv[m], vm, p.u[m]);
+      if constexpr (MOM)
+        if (p.u[m].v && p.u[m].g) stv(p.u[m].v + 4 * i, vm);
+      s = m == 0 ? y : add4(s, y);
+    }
+  }
   return s;
 }
-template <int M>
+template <int M, bool MOM>
 __device__ __forceinline__ float local_partial1(const XPart& p, int64_t j) {
-  float s = p.g[0] ? sgd1(p.x[0][j], p.g[0][j], p.lr[0]) : p.x[0][j];
+  float s = step1<MOM>(p.x[0][j], p.u[0], j);
 #pragma unroll
   for (int m = 1; m < M; ++m)
-    if (m < p.m) s = __fadd_rn(s, p.g[m] ? sgd1(p.x[m][j], p.g[m][j], p.lr[m]) : p.x[m][j]);
+    if (m < p.m) s = __fadd_rn(s, step1<MOM>(p.x[m][j], p.u[m], j));
   return s;
 }
 
@@ -154,7 +162,7 @@ __device__ __forceinline__ int64_t stage_off(const XPart& p, int d, int64_t i_re
   return (static_cast<int64_t>(d) * (p.S4 + 1) + i_rel) * 4;
 }
 
-template <int M, int U>
+template <int M, int U, bool MOM>
 __device__ void item_A(const XPart& p, int o, int64_t c) {
   const ChunkRange r = chunk_range(p, o, c);
   const int64_t slo = slice_lo(p, o);
@@ -164,7 +172,7 @@ __device__ void item_A(const XPart& p, int o, int64_t c) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
-      if (i < r.hi) s[u] = local_partial4<M>(p, i);
+      if (i < r.hi) s[u] = local_partial4<M, MOM>(p, i);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -174,11 +182,11 @@ __device__ void item_A(const XPart& p, int o, int64_t c) {
   }
   if (r.tail && threadIdx.x < p.rem) {
     const int64_t j = 4 * p.n4 + threadIdx.x;
-    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M>(p, j);
+    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M, MOM>(p, j);
   }
 }
 
-template <int M, int U>
+template <int M, int U, bool MOM>
 __device__ void item_B(const XPart& p, int64_t c) {
   const int o = p.me;
   const ChunkRange r = chunk_range(p, o, c);
@@ -190,7 +198,7 @@ __device__ void item_B(const XPart& p, int64_t c) {
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
       if (i < r.hi) {
-        const float4 mine = local_partial4<M>(p, i);
+        const float4 mine = local_partial4<M, MOM>(p, i);
         float4 part[kMaxXGpus];
 #pragma unroll
         for (int d = 0; d < kMaxXGpus; ++d)
@@ -212,7 +220,7 @@ __device__ void item_B(const XPart& p, int64_t c) {
   if (r.tail && threadIdx.x < p.rem) {
     const int64_t j = 4 * p.n4 + threadIdx.x;
     const int64_t so = p.n4 - slo;
-    const float mine = local_partial1<M>(p, j);
+    const float mine = local_partial1<M, MOM>(p, j);
     float s = o == 0 ? mine : stage[stage_off(p, 0, so) + threadIdx.x];
     for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == o ? mine : stage[stage_off(p, d, so) + threadIdx.x]);
     const float xbar = __fdiv_rn(s, kf);
@@ -251,10 +259,10 @@ __device__ void item_C(const XPart& p, int o, int64_t c) {
 }
 
 // L item: chunk c of fused intra-GPU group gi (alg1 steps 2+4 on one GPU, pinned fold)
-template <int K, int U>
+template <int K, int U, bool MOM>
 __device__ void item_L_k(const XLocalGroup& G, int64_t lo, int64_t hi, bool tail, int64_t n4, int rem) {
   for (int64_t t0 = lo; t0 < hi; t0 += kXThreads * U) {
-    float4 xv[U][K], gv[U][K];
+    float4 xv[U][K], gv[U][K], vv[U][MOM ? K : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
@@ -262,16 +270,24 @@ __device__ void item_L_k(const XLocalGroup& G, int64_t lo, int64_t hi, bool tail
 #pragma unroll
         for (int m = 0; m < K; ++m) {
           xv[u][m] = ldv(G.x[m] + 4 * i);
-          if (G.g[m]) gv[u][m] = ldg_nc(G.g[m] + 4 * i);
+          if (G.u[m].g) gv[u][m] = ldg_nc(G.u[m].g + 4 * i);
+          if constexpr (MOM)
+            if (G.u[m].v) vv[u][m] = ldv(G.u[m].v + 4 * i);
         }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
       if (i < hi) {
-        float4 s = G.g[0] ? sgd4(xv[u][0], gv[u][0], G.lr[0]) : xv[u][0];
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int m = 1; m < K; ++m) s = add4(s, G.g[m] ? sgd4(xv[u][m], gv[u][m], G.lr[m]) : xv[u][m]);
+        for (int m = 0; m < K; ++m) {
+          float4 vm = vv[u][MOM ? m : 0];
+          const float4 y = step4<MOM>(xv[u][m], gv[u][m], vm, G.u[m]);
+          if constexpr (MOM)
+            if (G.u[m].v && G.u[m].g) stv(G.u[m].v + 4 * i, vm);
+          s = m == 0 ? y : add4(s, y);
+        }
         if (K > 1) s = div4(s, static_cast<float>(K));
 #pragma unroll
         for (int m = 0; m < K; ++m) stv(G.x[m] + 4 * i, s);
@@ -280,14 +296,14 @@ __device__ void item_L_k(const XLocalGroup& G, int64_t lo, int64_t hi, bool tail
   }
   if (tail && threadIdx.x < rem) {
     const int64_t j = 4 * n4 + threadIdx.x;
-    float s = G.g[0] ? sgd1(G.x[0][j], G.g[0][j], G.lr[0]) : G.x[0][j];
-    for (int m = 1; m < K; ++m) s = __fadd_rn(s, G.g[m] ? sgd1(G.x[m][j], G.g[m][j], G.lr[m]) : G.x[m][j]);
+    float s = step1<MOM>(G.x[0][j], G.u[0], j);
+    for (int m = 1; m < K; ++m) s = __fadd_rn(s, step1<MOM>(G.x[m][j], G.u[m], j));
     if (K > 1) s = __fdiv_rn(s, static_cast<float>(K));
     for (int m = 0; m < K; ++m) G.x[m][j] = s;
   }
 }
 
-template <int U>
+template <int U, bool MOM>
 __device__ void item_L(const XTask& T, int64_t idx) {
   const XLocalGroup& G = T.lg[idx / T.nchl];
   const int64_t c = idx % T.nchl;
@@ -296,10 +312,10 @@ __device__ void item_L(const XTask& T, int64_t idx) {
   const int64_t lo = min(c * T.chl, n4), hi = min((c + 1) * T.chl, n4);
   const bool tail = (c == T.nchl - 1) && rem > 0;
   switch (G.k) {
-    case 1: item_L_k<1, U>(G, lo, hi, tail, n4, rem); break;
-    case 2: item_L_k<2, U>(G, lo, hi, tail, n4, rem); break;
-    case 3: item_L_k<3, U>(G, lo, hi, tail, n4, rem); break;
-    default: item_L_k<4, U>(G, lo, hi, tail, n4, rem); break;
+    case 1: item_L_k<1, U, MOM>(G, lo, hi, tail, n4, rem); break;
+    case 2: item_L_k<2, U, MOM>(G, lo, hi, tail, n4, rem); break;
+    case 3: item_L_k<3, U, MOM>(G, lo, hi, tail, n4, rem); break;
+    default: item_L_k<4, U, MOM>(G, lo, hi, tail, n4, rem); break;
   }
 }
 
@@ -317,7 +333,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // M bounds the local member count of every part (register budget).
-template <int M, int U>
+template <int M, int U, bool MOM>
 __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // READY: my staging is free for these groups (my previous kernel has finished)
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
     if (T.prof && threadIdx.x == 0) ts = gtimer();
     if (region == 3) {
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_L<1>(T, t);
+      item_L<1, MOM>(T, t);
       if (T.prof) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -361,7 +377,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
       }
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_A<M, U>(p, o, c);
+      item_A<M, U, MOM>(p, o, c);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -373,7 +389,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
           if (d != p.me) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, t), p.tag);
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_B<M, 1>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
+      item_B<M, 1, MOM>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -488,11 +504,12 @@ int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count
 }
 
 
-template <int M, int U>
+template <int M, int U, bool MOM = false>
 int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   static int occ = 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U>, kXThreads, 0) != cudaSuccess || occ < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U, MOM>, kXThreads, 0) != cudaSuccess ||
+        occ < 1)
       occ = 1;
   }
   if (g_sms == 0) {
@@ -521,7 +538,7 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   const int rc = item_list(T, cap, &T.items, &T.total_items, err);
   if (rc != RP_OK) return rc;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.total_items)));
-  xgpu_kernel<M, U><<<blocks, kXThreads, 0, stream>>>(T);
+  xgpu_kernel<M, U, MOM><<<blocks, kXThreads, 0, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("xgpu kernel launch: ") + cudaGetErrorString(e);
@@ -557,7 +574,8 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
       return RP_EINVAL;
     }
     for (int m = 0; m < G.k; ++m)
-      if (!G.x[m] || (reinterpret_cast<uintptr_t>(G.x[m]) & 15) || (reinterpret_cast<uintptr_t>(G.g[m]) & 15)) {
+      if (!G.x[m] || (reinterpret_cast<uintptr_t>(G.x[m]) & 15) || (reinterpret_cast<uintptr_t>(G.u[m].g) & 15) ||
+          (reinterpret_cast<uintptr_t>(G.u[m].v) & 15)) {
         *err = "xgpu: local replica / gradient pointers must be non-null and 16-byte aligned";
         return RP_EINVAL;
       }
@@ -580,6 +598,17 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   // every cross part of a step is in ONE launch (two launches on one stream could
   // wait on each other across GPUs), so M is the largest local member count
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  bool mom = false;
+  for (int pi = 0; pi < T.nparts; ++pi)
+    for (int m = 0; m < T.part[pi].m; ++m) mom = mom || (T.part[pi].u[m].v && T.part[pi].u[m].g);
+  for (int gi = 0; gi < T.nlocal; ++gi)
+    for (int m = 0; m < T.lg[gi].k; ++m) mom = mom || (T.lg[gi].u[m].v && T.lg[gi].u[m].g);
+  if (mom) {  // momentum buffers: separate instantiations keep the plain path's registers
+    if (mmax <= 1) return launch_m<1, 1, true>(T, s, err);
+    if (mmax <= 2) return launch_m<2, 1, true>(T, s, err);
+    if (mmax <= 4) return launch_m<4, 1, true>(T, s, err);
+    return launch_m<8, 1, true>(T, s, err);
+  }
   if (g_u < 0) {
     g_u = env_int("RP_XGPU_U", 4);
     g_cps = env_int("RP_XGPU_CTAS_PER_SM", 0);

@@ -150,6 +150,8 @@ _SIGNATURES = {
     "rp_gg_release": (ctypes.c_int, [_CTX, ctypes.c_int64]),
     "rp_retire": (ctypes.c_int, [_CTX, ctypes.c_int32]),
     "rp_step": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float]),
+    "rp_step_momentum": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                         _P]),
     "rp_preduce": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(rp_group)]),
     "rp_barrier_free_wait": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64]),
     "rp_batch_begin": (ctypes.c_int, [_CTX]),
@@ -288,6 +290,11 @@ def rp_retire(ctx, w):
 
 def rp_step(ctx, w, grad, lr):
     _check(load_library().rp_step(ctx, w, _ptr(grad), ctypes.c_float(lr)), "rp_step")
+
+
+def rp_step_momentum(ctx, w, grad, lr, momentum, weight_decay, v):
+    _check(load_library().rp_step_momentum(ctx, w, _ptr(grad), ctypes.c_float(lr), ctypes.c_float(momentum),
+                                           ctypes.c_float(weight_decay), _ptr(v)), "rp_step_momentum")
 
 
 def rp_preduce(ctx, w, group):
@@ -437,6 +444,9 @@ class Context:
 
     def step(self, w, grad=None, lr=0.1):
         rp_step(self.handle, w, grad, lr)
+
+    def step_momentum(self, w, grad=None, lr=0.1, momentum=0.9, weight_decay=1e-4, v=None):
+        rp_step_momentum(self.handle, w, grad, lr, momentum, weight_decay, v)
 
     def preduce(self, w, group):
         rp_preduce(self.handle, w, group)

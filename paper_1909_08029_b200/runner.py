@@ -33,7 +33,7 @@ def _ceil_to(v, m):
 class LockstepRunner:
     def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
                  lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True,
-                 peer_group=None):
+                 peer_group=None, section_length=1, momentum=None):
         if mode not in ("static", "gd"):
             raise ValueError("mode must be 'static' or 'gd'")
         if mode == "static" and rule not in RULES:
@@ -43,6 +43,8 @@ class LockstepRunner:
         self.device = rank if device is None else device
         torch.cuda.set_device(self.device)
         self.mode, self.rule, self.lr, self.grad_mode = mode, rule, lr, grad_mode
+        self.section_length = max(1, int(section_length))   # iterations between syncs
+        self.momentum = momentum                              # (mu, weight_decay)
         self.world, self.n = world, n_params
         self.n_gpus, self.peer_group = n_gpus, peer_group
         self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device,
@@ -52,6 +54,8 @@ class LockstepRunner:
         dev = torch.device("cuda", self.device)
         self.X = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
         self.G = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
+        self.V = (torch.zeros((len(self.local), self.ld), dtype=torch.float32, device=dev)
+                  if momentum is not None else None)
         self.streams = {}
         for i, w in enumerate(self.local):
             self.ctx.bind_worker(w, self.x(w), self.g(w))
@@ -78,6 +82,9 @@ class LockstepRunner:
     def g(self, w):
         return self.G[self._row(w), :self.n]
 
+    def v(self, w):
+        return self.V[self._row(w), :self.n]
+
     def init_replicas(self):
         for w in self.local:
             rp.fill_xi(self.x(w), self.n, SEED_X, w, 0, 0, self.streams[w])
@@ -90,6 +97,10 @@ class LockstepRunner:
     def groups_for_step(self, t):
         """Step 3 for every local worker; returns ({w: rp_group}, [seq of non-local GG groups])."""
         groups, foreign = {}, []
+        if t % self.section_length != 0:       # no synchronization this step: SGD only
+            for w in self.local:
+                groups[w] = rp.rp_group.make(-(1 + t * self.world + w), [w])
+            return groups, foreign
         if self.mode == "static":
             for w in self.local:
                 groups[w] = self.ctx.schedule_static_worker(RULES[self.rule], t, w)
@@ -110,12 +121,13 @@ class LockstepRunner:
         """One lockstep step; `grads` optionally maps w -> device tensor to use as g."""
         t = self.t + 1
         for w in self.local:
-            if grads is not None:
-                self.ctx.step(w, grads[w], self.lr)
+            g = grads[w] if grads is not None else None
+            if grads is None and self.grad_mode == "per_step":
+                rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, self.streams[w])
+            if self.momentum is not None:
+                self.ctx.step_momentum(w, g, self.lr, self.momentum[0], self.momentum[1], self.v(w))
             else:
-                if self.grad_mode == "per_step":
-                    rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, self.streams[w])
-                self.ctx.step(w, None, self.lr)
+                self.ctx.step(w, g, self.lr)
         groups, foreign = self.groups_for_step(t)
         self.ctx.batch_begin()
         try:

@@ -30,8 +30,10 @@ def main():
     ii = bool(getattr(a, "ii", False))
     nodes = ngpu if (a.rule == "paper4" or ii) else 0
     import paper_1909_08029_b200 as rp
+    mom = tuple(a.momentum) if getattr(a, "momentum", None) else None
     r = LockstepRunner(world, a.n, mode=a.mode, rule=a.rule, group_size=a.k, n_gpus=ngpu, rank=rank,
-                       device=local_rank, nodes=nodes, flags=rp.RP_FLAG_INTER_INTRA if ii else 0)
+                       device=local_rank, nodes=nodes, flags=rp.RP_FLAG_INTER_INTRA if ii else 0, momentum=mom,
+                       section_length=getattr(a, "section_length", 1))
     log = r.run(a.steps)
     r.synchronize()
     slices = [(0, a.n)] if not a.sample else [(0, a.sample), (a.n // 2, a.n // 2 + a.sample),
@@ -40,7 +42,8 @@ def main():
     for lo, hi in slices:
         X, olog = sim.run_lockstep(world, a.n, a.steps, mode=a.mode, rule=a.rule, k=a.k, nodes=nodes,
                                    m=(world // nodes if nodes else None), workers_per_gpu=a.wpg, lo=lo, hi=hi,
-                                   ii_nodes=ngpu if ii else 0)
+                                   ii_nodes=ngpu if ii else 0, momentum=mom,
+                                   section_length=getattr(a, "section_length", 1))
         for w in r.local:
             got = r.x(w)[lo:hi].cpu().numpy()
             if not np.array_equal(got.view(np.uint32), X[w].view(np.uint32)):

@@ -57,6 +57,20 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("gpus,extra", [(2, dict(wpg=2, n=60_011, k=3, mode="static", rule="shift_k", steps=10,
+                                                 momentum=[0.9, 1e-4])),
+                                        (2, dict(wpg=4, n=30_001, k=3, mode="gd", steps=9, momentum=[0.9, 1e-4],
+                                                 section_length=2)),
+                                        (4, dict(wpg=2, n=40_003, k=3, mode="gd", steps=8, momentum=[0.9, 1e-4],
+                                                 ii=True))])
+def test_multi_gpu_momentum_section_length(gpus, extra):
+    # P:1274 momentum + weight decay fused into the cross-GPU kernel (buffers stay per worker);
+    # P:1312 section length; Inter-Intra groups
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, dict(sample=0, rule=None, **extra))
+
+
 @pytest.mark.parametrize("gpus,wpg,n,k,mode,rule,steps,sample", CASES)
 def test_multi_gpu_parity(gpus, wpg, n, k, mode, rule, steps, sample):
     if _ngpu() < gpus:

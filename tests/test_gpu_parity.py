@@ -120,3 +120,28 @@ def test_inter_intra_one_gpu():
     assert olog[1][1] == [tuple(range(8))]               # the Intra step: one whole-node group
     _compare(r, X)
     r.close()
+
+
+@pytest.mark.parametrize("mode,k,kw", [("static", 2, dict(rule="shift_k")), ("gd", 3, dict())])
+def test_momentum_weight_decay_bit_exact(mode, k, kw):
+    # P:1274 optimizer (momentum 0.9, weight decay 1e-4) fused into the P-Reduce pass
+    n, T = 50_003, 25
+    world = 4 if mode == "static" else 8
+    r = LockstepRunner(world, n, mode=mode, group_size=k, momentum=(0.9, 1e-4), **kw)
+    r.run(T)
+    r.synchronize()
+    X, _ = sim.run_lockstep(world, n, T, mode=mode, k=k, momentum=(0.9, 1e-4), **kw)
+    _compare(r, X)
+    r.close()
+
+
+def test_section_length_bit_exact():
+    # synchronize every 3rd iteration only
+    n, T = 40_001, 13
+    r = LockstepRunner(4, n, mode="static", rule="shift_k", group_size=2, section_length=3)
+    log = r.run(T)
+    r.synchronize()
+    X, olog = sim.run_lockstep(4, n, T, mode="static", rule="shift_k", k=2, section_length=3)
+    assert [g for _, g in log] == [sorted(gs) for _, gs in olog]
+    _compare(r, X)
+    r.close()

@@ -117,3 +117,37 @@ def test_replay_rejects_forged_grant():
             break
     with pytest.raises(Exception):
         sim.replay_trace(events, 4, 64, k=2, c_thres=0, seed_gd=3)
+
+
+def test_section_length_only_syncs_every_L_steps():
+    # with section length L, steps t % L != 0 are SGD only
+    X, log = sim.run_lockstep(4, 256, 8, mode="static", rule="shift_k", k=2, section_length=4)
+    for t, groups in log:
+        if t % 4:
+            assert all(len(g) == 1 for g in groups)
+        else:
+            assert any(len(g) == 2 for g in groups)
+    # L = 1 reproduces the plain run
+    X1, _ = sim.run_lockstep(4, 256, 8, mode="static", rule="shift_k", k=2, section_length=1)
+    X0, _ = sim.run_lockstep(4, 256, 8, mode="static", rule="shift_k", k=2)
+    assert all(np.array_equal(X1[w], X0[w]) for w in range(4))
+
+
+def test_momentum_run_matches_fp64_reference():
+    # momentum + weight decay trajectory vs an independent fp64 loop
+    n, N, T, mu, wd = 4, 512, 30, 0.9, 1e-4
+    X, _ = sim.run_lockstep(n, N, T, mode="static", rule="shift_k", k=2, momentum=(mu, wd))
+    eta = float(np.float32(0.1))
+    mu64, wd64 = float(np.float32(mu)), float(np.float32(wd))
+    Y = np.stack([gen.x0(w, N).astype(np.float64) for w in range(n)], axis=1)
+    Vm = np.zeros_like(Y)
+    for t in range(1, T + 1):
+        Gt = np.stack([gen.grad(w, t, N).astype(np.float64) for w in range(n)], axis=1)
+        Vm = mu64 * Vm + (Gt + wd64 * Y)
+        Y = Y - eta * Vm
+        W = np.eye(n)
+        for g in S.shift_k(n, 2, t):
+            W = W @ A.group_matrix(n, g)
+        Y = A.apply(Y, W)
+    got = np.stack([X[w] for w in range(n)], axis=1).astype(np.float64)
+    assert np.max(np.abs(got - Y)) <= 2e-6 * np.abs(Y).max()

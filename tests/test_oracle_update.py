@@ -145,3 +145,48 @@ def test_exact_small_case_against_rationals():
     for w in x:
         for j in range(2):
             assert X[w][j] == F32(float(mean[j]))   # sum exact, one rounding in the divide
+
+
+def test_momentum_reduces_to_sgd():
+    # mu = 0, wd = 0: the momentum form is plain SGD bit for bit
+    rng = np.random.default_rng(7)
+    x, g = (rng.standard_normal(4096).astype(F32) for _ in range(2))
+    v = rng.standard_normal(4096).astype(F32)
+    y, v2 = U.momentum_sgd_fp32(x, g, v, LR, 0.0, 0.0)
+    assert np.array_equal(y, U.sgd_fp32(x, g, LR)) and np.array_equal(v2, g)
+
+
+def test_momentum_constant_gradient_closed_form():
+    # constant g, wd = 0, v0 = 0: v_t = g (1 - mu^t) / (1 - mu) (geometric series) and
+    # x_t = x0 - lr * sum_s v_s; checked against the closed form in fp64
+    mu, lr, T = 0.9, 0.1, 60
+    x0 = np.linspace(-1, 1, 1001).astype(F32)
+    g = np.full(1001, 0.25, F32)
+    x, v = x0.copy(), np.zeros(1001, F32)
+    for _ in range(T):
+        x, v = U.momentum_sgd_fp32(x, g, v, lr, mu, 0.0)
+    t = np.arange(1, T + 1)
+    vs = 0.25 * (1 - np.float64(np.float32(mu)) ** t) / (1 - np.float64(np.float32(mu)))
+    assert np.allclose(v, vs[-1], rtol=2e-6)
+    assert np.allclose(x, x0.astype(np.float64) - np.float64(np.float32(lr)) * vs.sum(), atol=2e-5)
+
+
+def test_weight_decay_shrinks_toward_zero():
+    # g = 0, mu = 0: x <- x - lr*wd*x = (1 - lr*wd) x, per step
+    x = np.linspace(-3, 3, 101).astype(F32)
+    y, _ = U.momentum_sgd_fp32(x, np.zeros_like(x), np.zeros_like(x), 0.5, 0.0, 0.1)
+    assert np.allclose(y, x * (1 - 0.05), atol=1e-6)
+
+
+def test_fused_update_with_momentum_buffers_stay_local():
+    # only the weights are averaged; every member keeps its own momentum buffer
+    rng = np.random.default_rng(8)
+    X = {w: rng.standard_normal(512).astype(F32) for w in range(3)}
+    G = {w: rng.standard_normal(512).astype(F32) for w in range(3)}
+    V = {w: rng.standard_normal(512).astype(F32) for w in range(3)}
+    V0 = {w: V[w].copy() for w in V}
+    ys = {w: U.momentum_sgd_fp32(X[w], G[w], V0[w], LR, 0.9, 1e-4) for w in range(3)}
+    U.fused_group_update(X, G, [0, 1, 2], LR, V=V, mu=0.9, wd=1e-4)
+    assert np.array_equal(X[0], ((ys[0][0] + ys[1][0]) + ys[2][0]) / F32(3))
+    for w in range(3):
+        assert np.array_equal(V[w], ys[w][1])
