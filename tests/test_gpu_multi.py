@@ -68,7 +68,7 @@ def test_multi_gpu_momentum_section_length(gpus, extra):
     # P:1312 section length; Inter-Intra groups
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
-    _run(gpus, dict(sample=0, rule=None, **extra))
+    _run(gpus, {"sample": 0, "rule": None, **extra})
 
 
 @pytest.mark.parametrize("gpus,wpg,n,k,mode,rule,steps,sample", CASES)
