@@ -11,7 +11,8 @@
 //  A (o, c)  o != me: p = left fold over my local members of
 //            y_m = fl(x_m - fl(lr_m g_m)) (ascending worker id) for chunk c of
 //            slice o, STORED OVER NVLINK into owner o's staging buffer (row me),
-//            then flag A[me][c] on owner o.
+//            then flag A[me][c] on owner o. By default each 256*U-float4 tile is
+//            staged in shared memory and pushed by the TMA (cp.async.bulk).
 //  B (c)     my slice: wait for A[d][c] from every peer d; own partial in
 //            registers, peers' partials from my staging (local HBM); s = left
 //            fold of the partials in ascending GPU id; xbar = fl(s / |G|)
@@ -230,6 +231,117 @@ __device__ void item_B(const XPart& p, int64_t c) {
   }
 }
 
+// ---- TMA bulk-store variants of A and B (RP_XGPU_TMA=1) ---------------------------------
+// The tile is staged in shared memory and one thread hands it to the Tensor Memory
+// Accelerator (cp.async.bulk global <- shared::cta): one bulk transfer per 256*U float4
+// instead of 256*U 16-byte peer stores; double-buffered; the flag follows
+// cp.async.bulk.wait_group 0 + an async-proxy fence + a system fence.
+__device__ __forceinline__ void bulk_store(void* dst_global, const void* src_smem, uint32_t bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(src_smem));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_global), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+template <int M, int U, bool MOM>
+__device__ void item_A_tma(const XPart& p, int o, int64_t c, float4* smem) {
+  const ChunkRange r = chunk_range(p, o, c);
+  const int64_t slo = slice_lo(p, o);
+  float* dst = p.stage[o];
+  constexpr int kTile = kXThreads * U;
+  int buf = 0;
+  for (int64_t t0 = r.lo; t0 < r.hi; t0 += kTile) {
+    if (threadIdx.x == 0) bulk_wait_read1();  // the transfer issued two tiles ago has read `buf`
+    __syncthreads();
+    float4* sb = smem + buf * kTile;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) sb[u * kXThreads + threadIdx.x] = local_partial4<M, MOM>(p, i);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t cnt = min(static_cast<int64_t>(kTile), r.hi - t0);
+      bulk_store(dst + stage_off(p, p.me, t0 - slo), sb, static_cast<uint32_t>(cnt * 16));  // NVLink
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+  if (r.tail && threadIdx.x < p.rem) {
+    const int64_t j = 4 * p.n4 + threadIdx.x;
+    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M, MOM>(p, j);
+  }
+  if (threadIdx.x == 0) {
+    bulk_wait_all();
+    fence_async_all();
+  }
+}
+
+template <int M, int U, bool MOM>
+__device__ void item_B_tma(const XPart& p, int64_t c, float4* smem) {
+  const int o = p.me;
+  const ChunkRange r = chunk_range(p, o, c);
+  const int64_t slo = slice_lo(p, o);
+  const float* stage = p.stage[o];
+  const float kf = static_cast<float>(p.k_total);
+  constexpr int kTile = kXThreads * U;
+  int buf = 0;
+  for (int64_t t0 = r.lo; t0 < r.hi; t0 += kTile) {
+    if (threadIdx.x == 0) bulk_wait_read1();
+    __syncthreads();
+    float4* sb = smem + buf * kTile;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = t0 + u * kXThreads + threadIdx.x;
+      if (i < r.hi) {
+        const float4 mine = local_partial4<M, MOM>(p, i);
+        float4 part[kMaxXGpus];
+#pragma unroll
+        for (int d = 0; d < kMaxXGpus; ++d)
+          if (d < p.kp && d != o) part[d] = ldv(stage + stage_off(p, d, i - slo));
+        float4 s = o == 0 ? mine : part[0];
+#pragma unroll
+        for (int d = 1; d < kMaxXGpus; ++d)
+          if (d < p.kp) s = add4(s, d == o ? mine : part[d]);
+        const float4 xbar = div4(s, kf);
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          if (m < p.m) stv(p.x[m] + 4 * i, xbar);
+        sb[u * kXThreads + threadIdx.x] = xbar;
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTile), r.hi - t0) * 16);
+      for (int d = 0; d < p.kp; ++d)
+        if (d != o) bulk_store(p.xfirst[d] + 4 * t0, sb, bytes);  // NVLink
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+  if (r.tail && threadIdx.x < p.rem) {
+    const int64_t j = 4 * p.n4 + threadIdx.x;
+    const int64_t so = p.n4 - slo;
+    const float mine = local_partial1<M, MOM>(p, j);
+    float s = o == 0 ? mine : stage[stage_off(p, 0, so) + threadIdx.x];
+    for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == o ? mine : stage[stage_off(p, d, so) + threadIdx.x]);
+    const float xbar = __fdiv_rn(s, kf);
+    for (int m = 0; m < p.m; ++m) p.x[m][j] = xbar;
+    for (int d = 0; d < p.kp; ++d)
+      if (d != o) p.xfirst[d][j] = xbar;
+  }
+  if (threadIdx.x == 0) {
+    bulk_wait_all();
+    fence_async_all();
+  }
+}
+
 template <int M, int U>
 __device__ void item_C(const XPart& p, int o, int64_t c) {
   if (p.m == 1) return;  // the owner stored xbar straight into my only replica
@@ -333,8 +445,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // M bounds the local member count of every part (register budget).
-template <int M, int U, bool MOM>
+template <int M, int U, bool MOM, bool TMA>
 __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
+  extern __shared__ float4 xsmem[];  // TMA: two tiles of kXThreads * U float4
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // READY: my staging is free for these groups (my previous kernel has finished)
     for (int pi = 0; pi < T.nparts; ++pi) {
@@ -377,7 +490,10 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
       }
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_A<M, U, MOM>(p, o, c);
+      if constexpr (TMA)
+        item_A_tma<M, U, MOM>(p, o, c, xsmem);
+      else
+        item_A<M, U, MOM>(p, o, c);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -389,7 +505,10 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
           if (d != p.me) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, t), p.tag);
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_B<M, 1, MOM>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
+      if constexpr (TMA)
+        item_B_tma<M, U, MOM>(p, t, xsmem);
+      else
+        item_B<M, 1, MOM>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -426,7 +545,7 @@ int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : def;
 }
-int g_u = -1, g_cps = -1, g_lag = -1, g_order = -1;
+int g_u = -1, g_cps = -1, g_lag = -1, g_order = -1, g_tma = -1;
 int64_t g_min_chunk = -1;
 
 // Host-built work-item order, cached per launch shape. Virtual time in units of a
@@ -504,11 +623,13 @@ int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count
 }
 
 
-template <int M, int U, bool MOM = false>
+template <int M, int U, bool MOM = false, bool TMA = false>
 int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   static int occ = 0;
+  const size_t smem = TMA ? 2 * sizeof(float4) * kXThreads * U : 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U, MOM>, kXThreads, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U, MOM, TMA>, kXThreads, smem) !=
+            cudaSuccess ||
         occ < 1)
       occ = 1;
   }
@@ -538,7 +659,7 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   const int rc = item_list(T, cap, &T.items, &T.total_items, err);
   if (rc != RP_OK) return rc;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.total_items)));
-  xgpu_kernel<M, U, MOM><<<blocks, kXThreads, 0, stream>>>(T);
+  xgpu_kernel<M, U, MOM, TMA><<<blocks, kXThreads, smem, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("xgpu kernel launch: ") + cudaGetErrorString(e);
@@ -603,17 +724,31 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
     for (int m = 0; m < T.part[pi].m; ++m) mom = mom || (T.part[pi].u[m].v && T.part[pi].u[m].g);
   for (int gi = 0; gi < T.nlocal; ++gi)
     for (int m = 0; m < T.lg[gi].k; ++m) mom = mom || (T.lg[gi].u[m].v && T.lg[gi].u[m].g);
-  if (mom) {  // momentum buffers: separate instantiations keep the plain path's registers
-    if (mmax <= 1) return launch_m<1, 1, true>(T, s, err);
-    if (mmax <= 2) return launch_m<2, 1, true>(T, s, err);
-    if (mmax <= 4) return launch_m<4, 1, true>(T, s, err);
-    return launch_m<8, 1, true>(T, s, err);
-  }
   if (g_u < 0) {
     g_u = env_int("RP_XGPU_U", 4);
     g_cps = env_int("RP_XGPU_CTAS_PER_SM", 0);
     g_lag = env_int("RP_XGPU_LAG", 0);
     g_order = env_int("RP_XGPU_ORDER", 0);
+    g_tma = env_int("RP_XGPU_TMA", 1);
+  }
+  if (mom) {  // momentum buffers: separate instantiations keep the plain path's registers
+    if (g_tma > 0) {
+      if (mmax <= 1) return launch_m<1, 1, true, true>(T, s, err);
+      if (mmax <= 2) return launch_m<2, 1, true, true>(T, s, err);
+      if (mmax <= 4) return launch_m<4, 1, true, true>(T, s, err);
+      return launch_m<8, 1, true, true>(T, s, err);
+    }
+    if (mmax <= 1) return launch_m<1, 1, true>(T, s, err);
+    if (mmax <= 2) return launch_m<2, 1, true>(T, s, err);
+    if (mmax <= 4) return launch_m<4, 1, true>(T, s, err);
+    return launch_m<8, 1, true>(T, s, err);
+  }
+  if (g_tma > 0) {  // default: TMA bulk stores for the NVLink pushes (+17-31 % on 2 B200,
+                    // profiles/r01_xgpu_tma_sweep_2gpu.txt); RP_XGPU_TMA=0 selects peer STG.128
+    if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4, false, true>(T, s, err) : launch_m<1, 2, false, true>(T, s, err);
+    if (mmax <= 2) return launch_m<2, 2, false, true>(T, s, err);
+    if (mmax <= 4) return launch_m<4, 1, false, true>(T, s, err);
+    return launch_m<8, 1, false, true>(T, s, err);
   }
   if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4>(T, s, err) : (g_u == 1 ? launch_m<1, 1>(T, s, err) : launch_m<1, 2>(T, s, err));
   if (mmax <= 2) return g_u == 1 ? launch_m<2, 1>(T, s, err) : launch_m<2, 2>(T, s, err);  // U=4 spills
