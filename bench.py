@@ -218,7 +218,7 @@ def run_ours(args, wl):
     hbm_roof = None
     if loc_ms > 0:
         a = loc_b / (loc_ms / 1e3) / 1e9
-        hbm_roof = {"bound": "hbm", "kernel": "preduce_multi_kernel (fused SGD + P-Reduce, intra-GPU groups)",
+        hbm_roof = {"bound": "hbm", "kernel": "preduce_tma_kernel (fused SGD + P-Reduce, intra-GPU groups, TMA bulk copies)",
                     "achieved": round(a, 1), "peak": peaks["hbm_gbs"], "peak_source": peak_src, "unit": "GB/s",
                     "frac": round(a / peaks["hbm_gbs"], 4),
                     "traffic": traffic_from_profiles(args.workload, n_gpus),

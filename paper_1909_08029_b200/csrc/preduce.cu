@@ -247,6 +247,17 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     const char* v = std::getenv("RP_PREDUCE_MINB");
     minb = v && *v ? std::atoi(v) : 0;
   }
+  // TMA bulk-copy pipeline (preduce_tma.cu) by default: variant 3 won the sweep in
+  // profiles/r01_tma_local_sweep.txt; RP_PREDUCE_TMA=0 selects this file's LDG/STG kernel.
+  static int use_tma = -1;
+  if (use_tma < 0) {
+    const char* v = std::getenv("RP_PREDUCE_TMA");
+    use_tma = v && *v ? std::atoi(v) : 3;
+  }
+  if (use_tma > 0) {
+    const int rc = launch_preduce_tma(t, n, stream, err, use_tma);
+    if (rc != RP_EINVAL) return rc;
+  }
   bool mom = false;
   for (int i = 0; i < nm; ++i) mom = mom || (t.u[i].v != nullptr && t.u[i].g != nullptr);
   if (mom) {  // momentum buffers: a separate instantiation keeps the plain path's registers
