@@ -509,12 +509,12 @@ def oracle_steps(wl, n_gpus, sample, steps):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(wl, n_gpus, budget_s=15.0):
+def cpu_baseline(wl, n_gpus, budget_s=12.0):
     """The oracle as it stands, one host core, bounded sample scaled to the full vector."""
     world = wl["wpg"] * n_gpus
     sample = min(wl["n"], 1 << 20)
     dt = oracle_steps(wl, n_gpus, sample, 1)                        # calibrate
-    steps = max(1, min(50, int(budget_s / max(dt, 1e-6))))
+    steps = max(1, min(2000, int(budget_s / max(dt, 1e-6))))
     dt = oracle_steps(wl, n_gpus, sample, steps)
     value = world * steps / dt * (sample / wl["n"])
     return {"value": round(value, 3), "unit": "worker-steps/s", "cores": 1, "kind": "oracle",
