@@ -178,7 +178,8 @@ def run_ours(args, wl):
     flags = rp.RP_FLAG_TIMING | (rp.RP_FLAG_INTER_INTRA if wl.get("inter_intra") else 0)
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
                             rank=rank, device=local_rank, grad_mode="resident", flags=flags,
-                            nodes=n_gpus if wl.get("inter_intra") else 0, peer_group=pg)
+                            nodes=n_gpus if wl.get("inter_intra") else 0, peer_group=pg,
+                            nvls=args.nvls if n_gpus > 1 else 0)
     for _ in range(args.warmup):
         runner.step()
     runner.synchronize()
@@ -233,7 +234,10 @@ def run_ours(args, wl):
         xh = sum(r["tim"]["cross_bytes_hbm"] for r in per_rank)
         ah = xh / (x_ms / 1e3) / 1e9
         nl = sum(r["tim"]["cross_launches"] for r in per_rank)
-        nvl_roof = {"bound": "nvlink", "kernel": "xgpu_kernel (fused SGD + P-Reduce, cross-GPU part)",
+        kname = "xgpu_kernel (fused SGD + P-Reduce, cross-GPU part)"
+        if args.nvls:
+            kname = f"nvls_kernel (in-switch P-Reduce, groups on >= {args.nvls} GPUs) + " + kname
+        nvl_roof = {"bound": "nvlink", "kernel": kname,
                     "achieved": round(a, 1), "peak": NVLINK_PEAK,
                     "peak_source": "fallback (B200_PROFILING.md: measured peer copy per direction; 900 nominal)",
                     "unit": "GB/s", "frac": round(a / NVLINK_PEAK, 4), "frac_of_nominal": round(a / NVLINK_NOMINAL, 4),
@@ -271,6 +275,7 @@ def run_ours(args, wl):
                    "n_params": n, "group_size": k, "schedule": wl["rule"] or "GB+GD (lockstep, ascending requests)",
                    "lr": 0.1, "hbm_bytes_per_step": int(hbm_step), "nvlink_bytes_per_step": int(nvl_step),
                    "cross_gpu_groups_per_step": sum(r["cross"] for r in per_rank) / args.steps,
+                   "nvls_min_gpus": args.nvls if n_gpus > 1 else 0,
                    "parallelism": f"{n_gpus} ranks x {wpg} workers, disjoint groups",
                    "l2": ("inputs larger than L2" if hbm_step / n_gpus > L2_BYTES else
                           "working set fits in L2 (no flush): L2-resident number")},
@@ -309,7 +314,8 @@ def run_async(args, wl):
     if args.k:
         k = min(args.k, world)
     r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
-                    job_id=job[0], peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg)
+                    job_id=job[0], peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg,
+                    nvls=args.nvls if n_gpus > 1 else 0)
     tc = int(args.tc_us * 1000)
     slow = float(args.slow)
 
@@ -318,7 +324,8 @@ def run_async(args, wl):
     r.run(steps=max(3, args.warmup), delay_ns=delay, delay_mode=args.delay)   # warm-up, then all retired
     r.close()
     r = AsyncRunner(world, n, group_size=k, c_thres=4, seed_gd=3, n_gpus=n_gpus, rank=rank, device=local_rank,
-                    job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg)
+                    job_id=job[0] + 1, peer_group=pg, grad_mode="resident", flags=rp.RP_FLAG_TIMING, policy=args.gg,
+                    nvls=args.nvls if n_gpus > 1 else 0)
     barrier(pg)
     with ClockSampler(local_rank) as clk:
         done = r.run(window_s=args.window, delay_ns=delay, delay_mode=args.delay)
@@ -571,6 +578,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--nvls", type=int, default=0,
+                    help="N>1: cross-GPU groups spanning >= this many GPUs reduce inside the NVSwitch (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
     ap.add_argument("--tc-us", type=float, default=2000.0, help="cfg5: synthetic compute time per step")

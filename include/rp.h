@@ -122,6 +122,7 @@ typedef struct rp_stats {
   int64_t bytes_nvlink;       /* algorithmic NVLink bytes stored by this GPU            */
   int64_t gg_pending;         /* random GG: requests whose group had to wait (conflicts) */
   int64_t gg_granted;         /* random GG: groups granted                              */
+  int64_t nvls_groups;        /* cross-GPU groups reduced in the NVSwitch (rp_nvls_enable) */
 } rp_stats;
 
 /* Device time of this context's P-Reduce kernel launches (RP_FLAG_TIMING),
@@ -198,6 +199,41 @@ int rp_peer_export(rp_ctx* ctx, rp_peer_info* out);
 /* Map the peers' memory (infos[i] for every rank i, own record ignored).
  * Errors: RP_EINVAL (missing / inconsistent records), RP_ECUDA. */
 int rp_peer_import(rp_ctx* ctx, const rp_peer_info* infos, int32_t n);
+
+/* ---- multi-GPU: NVLS (NVLink SHARP) P-Reduce, SURVEY §8 row f1 ------------------------
+ * The averaging of alg1 step 4 for a group spanning kp GPUs, reduced INSIDE
+ * the NVSwitch: every GPU writes its local partial (its members' SGD-updated replicas,
+ * left-folded, reading R1) into a buffer bound to a multicast object of the group's GPU
+ * set; the owner of each chunk reads the sum of all kp partials with one
+ * multimem.ld_reduce, divides by |G| and writes the mean to every GPU with one
+ * multimem.st. Per-GPU NVLink bytes are ~4N per direction for any kp (the push kernel
+ * moves 2(kp-1)/kp * 4N). The multicast objects play the role of the paper's cached
+ * per-group NCCL communicators (at most 64 cached); one object (with
+ * workers_per_gpu slots of ~4N bytes) per GPU subset of >= min_gpus GPUs, created once.
+ * The switch's summation order over the kp partials is its own (reading R25): results
+ * are bit-exact to the oracle for kp = 2 (fp32 addition is commutative) and within the
+ * north-star tolerance otherwise. */
+
+/* *supported = 1 when this rank's GPU supports multicast objects (driver + NVSwitch
+ * fabric), else 0. Errors: RP_ESTATE (not a multi-GPU context). */
+int rp_nvls_supported(rp_ctx* ctx, int32_t* supported);
+
+/* Collective-barrier callback for rp_nvls_enable: must block until every rank of the
+ * context has called it the same number of times, and return 0 iff every rank passed
+ * local_status == 0 (an all-reduce of the ranks' status; nonzero = some rank failed). */
+typedef int (*rp_barrier_fn)(void* user, int32_t local_status);
+
+/* Collective over ALL ranks, after rp_peer_import, before the first rp_preduce: create,
+ * share (POSIX file descriptors over a Unix socket, creator = lowest GPU of the subset)
+ * and bind the multicast objects of every GPU subset of >= min_gpus (2..n_gpus) GPUs,
+ * then route cross-GPU groups spanning >= min_gpus GPUs through the NVLS kernel.
+ * `barrier(user, status)` is called 3 times by every rank; a rank's failure makes every
+ * rank stop and return an error (nobody waits on a missing member). Device memory: per subset
+ * workers_per_gpu * (4 n_params + flags) bytes on every GPU of the subset.
+ * Errors: RP_EINVAL (min_gpus out of range, > 64 subsets), RP_ESTATE (peers not
+ * imported, already enabled), RP_ENODEV (no multicast support), RP_ECUDA, RP_ENOMEM.
+ * On error NVLS stays disabled (the push kernel keeps every group). */
+int rp_nvls_enable(rp_ctx* ctx, int32_t min_gpus, rp_barrier_fn barrier, void* user);
 
 /* ---- Step 3: group determination -------------------------------------------------- */
 

@@ -36,7 +36,7 @@ def _ceil_to(v, m):
 class AsyncRunner:
     def __init__(self, world, n_params, *, group_size, c_thres=4, seed_gd=3, n_gpus=1, rank=0, device=None,
                  lr=0.1, job_id=0, peer_group=None, trace_path=None, grad_mode="per_step", flags=0,
-                 policy="gd"):
+                 policy="gd", nvls=0):
         if grad_mode not in ("per_step", "resident"):
             raise ValueError("grad_mode must be 'per_step' or 'resident'")
         self.device = rank if device is None else device
@@ -62,6 +62,8 @@ class AsyncRunner:
             self.streams[w] = self.ctx.worker_stream(w)
         if n_gpus > 1:
             self.ctx.peer_setup(peer_group)
+            if nvls:   # groups spanning >= nvls GPUs reduce inside the NVSwitch (rp_nvls_enable)
+                self.ctx.nvls_enable(nvls, peer_group)
         if trace_path:
             self.ctx.trace_open(trace_path)
         for w in self.local:

@@ -163,6 +163,8 @@ struct rp_ctx {
   int64_t prof_cap = 0, prof_items = 0;
   std::string prof_path;
   std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
+  int32_t peer_pid[RP_MAX_GPUS] = {};               // process ids (NVLS descriptor sockets)
+  rp::NvlsState nvls;                               // multicast objects (rp_nvls_enable)
 };
 
 namespace {
@@ -246,13 +248,27 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // ordered after the kernel and records its own completion event.
 int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
                  cudaStream_t stream);
+int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream);
 int pump_cross(rp_ctx* c);
+
+// GPU subset of a group, and whether it takes the NVLS path (rp_nvls_enable).
+uint32_t gpu_mask(const rp_ctx* c, const rp_group& g) {
+  uint32_t m = 0;
+  for (int i = 0; i < g.size; ++i) m |= 1u << (g.members[i] / c->cfg.workers_per_gpu);
+  return m;
+}
+bool nvls_group(const rp_ctx* c, const rp_group& g) {
+  return c->nvls.min_gpus > 0 && __builtin_popcount(gpu_mask(c, g)) >= c->nvls.min_gpus;
+}
 int open_shared_gg(rp_ctx* c);
 
 int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (all_seqs.empty()) return RP_OK;
-  std::vector<int64_t> seqs, cross;
-  for (int64_t q : all_seqs) (c->active.at(q).local_mask == c->active.at(q).members_mask ? seqs : cross).push_back(q);
+  std::vector<int64_t> seqs, cross, nv;  // intra-GPU, push cross-GPU, NVLS cross-GPU
+  for (int64_t q : all_seqs) {
+    const ActiveGroup& a = c->active.at(q);
+    (a.local_mask == a.members_mask ? seqs : (nvls_group(c, a.g) ? nv : cross)).push_back(q);
+  }
   uint64_t all = 0;
   for (int64_t q : all_seqs) {
     ActiveGroup& a = c->active.at(q);
@@ -314,6 +330,12 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     }
     c->stats.kernel_launches++;
     c->stats.bytes_hbm += bytes;
+  }
+  // NVLS groups first, then the push kernel: every GPU issues its cross-GPU launches in
+  // the same order, so no launch waits on a peer's later launch
+  if (!nv.empty()) {
+    const int rc = launch_nvls_groups(c, nv, L.stream);
+    if (rc != RP_OK) return rc;
   }
   if (!cross.empty()) {
     const int rc = launch_cross(c, cross, fused, L.stream);
@@ -449,6 +471,81 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
   return RP_OK;
 }
 
+// This GPU's parts of every NVLS group of the batch, in ONE nvls launch (caller holds mu).
+// Slots: the k-th group launched on a GPU subset uses slot k mod slots with tag
+// k / slots + 1; every GPU of the subset launches the subset's groups in the same order
+// (ascending seq within a batch; batches in step order; asynchronous groups in ticket
+// order), so all agree on slot and tag.
+int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream) {
+  if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
+  if (static_cast<int>(seqs.size()) > rp::kMaxNParts)
+    return fail(RP_EINVAL, "more than 8 NVLS groups on one GPU in one step");
+  std::sort(seqs.begin(), seqs.end());
+  const int wpg = c->cfg.workers_per_gpu;
+  rp::NTask T{};
+  T.nparts = static_cast<int32_t>(seqs.size());
+  const int64_t n = c->cfg.n_params;
+  int64_t hbm = 0, nvl = 0;
+  for (size_t pi = 0; pi < seqs.size(); ++pi) {
+    ActiveGroup& a = c->active.at(seqs[pi]);
+    rp::NvlsObj* o = rp::nvls_find(&c->nvls, gpu_mask(c, a.g));
+    if (!o) return fail(RP_ESTATE, "no multicast object for the GPU subset of group " + std::to_string(a.g.seq));
+    rp::NPart& p = T.part[pi];
+    const int64_t use = o->launched++;
+    const int64_t slot = use % o->slots;
+    p.tag = static_cast<uint64_t>(use / o->slots) + 1;
+    p.kp = o->kp;
+    p.me = o->me;
+    p.k_total = a.g.size;
+    p.rem = static_cast<int32_t>(n % 4);
+    p.n4 = n / 4;
+    p.CH = o->CH;
+    p.nch = o->nch;
+    char* ucb = reinterpret_cast<char*>(o->uc_va) + slot * o->slot_bytes;
+    char* mcb = reinterpret_cast<char*>(o->mc_va) + slot * o->slot_bytes;
+    p.uc = reinterpret_cast<float*>(ucb);
+    p.mc = reinterpret_cast<float*>(mcb);
+    p.ucf = reinterpret_cast<unsigned long long*>(ucb + o->data_bytes);
+    p.mcf = reinterpret_cast<unsigned long long*>(mcb + o->data_bytes);
+    int64_t rd = 0;
+    for (int i = 0; i < a.g.size; ++i) {
+      const int m = a.g.members[i];
+      if (m / wpg != c->cfg.rank) continue;
+      if (p.m >= rp::kMaxXLocal) return fail(RP_EINVAL, "more than 8 local members in a cross-GPU group");
+      p.x[p.m] = c->w[m].x;
+      p.u[p.m] = a.u[i];
+      rd += member_bytes(a.u[i]) - 4;
+      p.m++;
+    }
+    // HBM: reads (x, g, v) + v writes, partial write, the switch's read of this copy and
+    // its write of the means, the owner's / copy-out stores of x, the copy-out reads
+    hbm += rd * n + 4 * n + 8 * n + 4 * p.m * n + 4 * n * (p.kp - 1) / p.kp;
+    nvl += 4 * n;  // per GPU and direction: ~4N for any kp
+    c->stats.nvls_groups++;
+    c->stats.groups_launched++;
+    c->stats.cross_gpu_groups++;
+  }
+  const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing) {
+    e0 = timing_event(c);
+    e1 = timing_event(c);
+    if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
+    CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  std::string err;
+  const int rc = rp::launch_nvls(T, stream, &err);
+  if (rc != RP_OK) return fail(rc, err);
+  if (timing) {
+    CUDA_TRY(cudaEventRecord(e1, stream));
+    c->timed.push_back({e0, e1, hbm, nvl, true});
+  }
+  c->stats.kernel_launches++;
+  c->stats.bytes_hbm += hbm;
+  c->stats.bytes_nvlink += nvl;
+  return RP_OK;
+}
+
 // Launch one asynchronous cross-GPU group on the comm stream (caller holds mu).
 int launch_cross_async(rp_ctx* c, int64_t seq) {
   ActiveGroup& a = c->active.at(seq);
@@ -458,7 +555,7 @@ int launch_cross_async(rp_ctx* c, int64_t seq) {
                                   " hold an unfinished group");
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if ((a.local_mask >> m) & 1) CUDA_TRY(cudaStreamWaitEvent(c->comm, c->w[m].ev_arrive, 0));
-  const int rc = launch_cross(c, {seq}, {}, c->comm);
+  const int rc = nvls_group(c, a.g) ? launch_nvls_groups(c, {seq}, c->comm) : launch_cross(c, {seq}, {}, c->comm);
   if (rc != RP_OK) return rc;
   WorkerSlot& L = c->w[__builtin_ctzll(a.local_mask)];
   CUDA_TRY(cudaEventRecord(L.ev_group, c->comm));
@@ -701,7 +798,7 @@ int rp_peer_export(rp_ctx* c, rp_peer_info* out) {
   out->rank = c->cfg.rank;
   out->n_local = wpg;
   out->first_worker = c->cfg.rank * wpg;
-  out->pid = 0;
+  out->pid = static_cast<int32_t>(getpid());
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, c->flags));
   std::memcpy(out->flags_handle, &h, sizeof(h));
@@ -756,6 +853,7 @@ int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
         r.stage_region_bytes != c->stage_region)
       return fail(RP_EINVAL, "rp_peer_import: inconsistent record for rank " + std::to_string(r.rank));
     seen[r.rank] = true;
+    c->peer_pid[r.rank] = r.pid;
     if (r.rank == c->cfg.rank) continue;
     void* fb = nullptr;
     int rc = open(r.flags_handle, &fb);
@@ -776,6 +874,34 @@ int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
   return RP_OK;
 }
 
+int rp_nvls_supported(rp_ctx* c, int32_t* supported) {
+  if (!c || !supported) return fail(RP_EINVAL, "null argument");
+  if (!c->has_gpu || c->cfg.n_gpus < 2) return fail(RP_ESTATE, "rp_nvls_supported: not a multi-GPU context");
+  cudaSetDevice(c->cfg.device);
+  int v = 0;
+  rp::nvls_supported(c->cfg.device, &v);
+  *supported = v;
+  return RP_OK;
+}
+
+int rp_nvls_enable(rp_ctx* c, int32_t min_gpus, rp_barrier_fn barrier, void* user) {
+  if (!c || !barrier) return fail(RP_EINVAL, "null argument");
+  if (!c->has_gpu || c->cfg.n_gpus < 2) return fail(RP_ESTATE, "rp_nvls_enable: not a multi-GPU context");
+  if (min_gpus < 2 || min_gpus > c->cfg.n_gpus) return fail(RP_EINVAL, "rp_nvls_enable: min_gpus out of range");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->peers_ready) return fail(RP_ESTATE, "rp_nvls_enable: call rp_peer_import first");
+  if (c->nvls.min_gpus > 0) return fail(RP_ESTATE, "rp_nvls_enable: already enabled");
+  int subsets = 0;
+  for (uint32_t m = 1; m < (1u << c->cfg.n_gpus); ++m) subsets += __builtin_popcount(m) >= min_gpus;
+  if (subsets > 64) return fail(RP_EINVAL, "rp_nvls_enable: more than 64 GPU subsets (P:1239 cache bound)");
+  cudaSetDevice(c->cfg.device);
+  std::string err;  // unsupported hardware fails inside, in step with the other ranks
+  const int rc = rp::nvls_setup(&c->nvls, c->cfg.rank, c->cfg.n_gpus, c->cfg.device, c->cfg.workers_per_gpu,
+                                c->cfg.n_params, min_gpus, c->peer_pid, barrier, user, &err);
+  if (rc != RP_OK) return fail(rc, err);
+  return RP_OK;
+}
+
 int rp_finalize(rp_ctx* c) {
   if (!c) return RP_OK;
   if (c->has_gpu) {
@@ -790,6 +916,8 @@ int rp_finalize(rp_ctx* c) {
       cudaStreamDestroy(c->comm);
     }
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+    cudaDeviceSynchronize();
+    rp::nvls_teardown(&c->nvls);
     if (c->flags) cudaFree(c->flags);
     if (c->stage) cudaFree(c->stage);
     if (c->prof) {

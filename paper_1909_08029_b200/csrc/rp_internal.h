@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "rp.h"
 
@@ -166,6 +167,58 @@ void xgpu_geometry(XPart& p, int64_t n);
 int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
+
+// ---- NVLS P-Reduce (nvls.cu kernel, nvls_setup.cpp multicast objects) ---------------------
+// One multicast object per GPU subset (mask of GPU ids, >= min_gpus GPUs), bound on every GPU
+// of the subset to `slots` slots of slot_bytes: slot data (4 n bytes: the GPU's partial, then
+// the mean) followed by flags [nch][kNvlsFlagStride] u64 (arrive[position], done).
+constexpr int kNvlsFlagStride = 9;   // arrive[8] + done
+constexpr int kMaxNParts = 8;        // NVLS groups one GPU takes part in, per launch
+struct NvlsObj {
+  uint32_t mask;         // GPU subset
+  int32_t kp, me;        // |subset|, this GPU's position (ascending GPU id)
+  int32_t slots;
+  int64_t slot_bytes, data_bytes, nch, CH;  // CH: chunk in float4
+  uint64_t mc_handle, mem_handle;           // CUmemGenericAllocationHandle
+  uintptr_t uc_va, mc_va;                   // unicast / multicast mappings of the whole object
+  size_t size;
+  int64_t launched;      // groups launched on this subset (slot = launched % slots)
+};
+struct NvlsState {
+  int32_t min_gpus = 0;  // 0 = disabled
+  std::vector<NvlsObj> objs;
+};
+int nvls_supported(int device, int* out);
+// Collective over all ranks (barrier called 3 times on every rank).
+int nvls_setup(NvlsState* s, int rank, int n_gpus, int device, int wpg, int64_t n, int min_gpus,
+               const int32_t* peer_pids, rp_barrier_fn barrier, void* user, std::string* err);
+void nvls_teardown(NvlsState* s);
+NvlsObj* nvls_find(NvlsState* s, uint32_t mask);
+int64_t nvls_chunk_f4();
+
+struct NPart {
+  int32_t m;             // local members (ascending worker id)
+  int32_t kp, me;        // GPUs in the group, this GPU's position
+  int32_t k_total;       // |G|
+  int32_t rem;           // n mod 4
+  uint64_t tag;          // nonzero; unique per use of the slot
+  int64_t n4, CH, nch, nown;
+  int64_t off_P, off_R, off_S;   // first item of each phase for this part
+  float* x[kMaxXLocal];
+  MemberUpdate u[kMaxXLocal];
+  float* uc;                     // slot data, this GPU's copy (unicast)
+  float* mc;                     // slot data, multicast address
+  unsigned long long* ucf;       // slot flags, unicast
+  unsigned long long* mcf;       // slot flags, multicast
+};
+struct NTask {
+  int32_t nparts;
+  int32_t hbm_ctas;              // CTAs on the P/S list (launcher); 0 = one list
+  int64_t total_items, n_p, n_r, off_s0, n_hbm;
+  NPart part[kMaxNParts];
+};
+// This GPU's parts of every NVLS group of one step, in ONE launch (items P*, R*, S*).
+int launch_nvls(NTask& t, void* stream, std::string* err);
 int launch_delay(void* stream, int64_t ns, std::string* err);
 int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                    void* stream, std::string* err);

@@ -85,7 +85,7 @@ class rp_stats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "groups_launched", "singleton_groups", "cross_gpu_groups", "kernel_launches", "gd_calls",
         "gg_requests", "max_gb_depth", "lock_assertions", "bytes_hbm", "bytes_nvlink", "gg_pending",
-        "gg_granted")]
+        "gg_granted", "nvls_groups")]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -131,6 +131,8 @@ class RPError(RuntimeError):
 
 _P = ctypes.c_void_p
 _CTX = ctypes.c_void_p
+# int (*rp_barrier_fn)(void* user, int32_t local_status)
+RP_BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32)
 # name -> (restype, argtypes); the list is also what the ABI test checks against rp.h
 _SIGNATURES = {
     "rp_init": (ctypes.c_int, [ctypes.POINTER(rp_config), ctypes.POINTER(_CTX)]),
@@ -140,6 +142,8 @@ _SIGNATURES = {
     "rp_set_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, _P]),
     "rp_peer_export": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_peer_info)]),
     "rp_peer_import": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_peer_info), ctypes.c_int32]),
+    "rp_nvls_supported": (ctypes.c_int, [_CTX, ctypes.POINTER(ctypes.c_int32)]),
+    "rp_nvls_enable": (ctypes.c_int, [_CTX, ctypes.c_int32, RP_BARRIER_FN, _P]),
     "rp_schedule_static": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "rp_schedule_static_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
@@ -246,6 +250,23 @@ def rp_peer_import(ctx, records):
     for i, b in enumerate(records):
         ctypes.memmove(ctypes.byref(arr[i]), b, ctypes.sizeof(rp_peer_info))
     _check(load_library().rp_peer_import(ctx, arr, len(records)), "rp_peer_import")
+
+
+def rp_nvls_supported(ctx):
+    out = ctypes.c_int32()
+    _check(load_library().rp_nvls_supported(ctx, ctypes.byref(out)), "rp_nvls_supported")
+    return bool(out.value)
+
+
+def rp_nvls_enable(ctx, min_gpus, barrier):
+    """barrier(status) -> bool: collective; True iff every rank passed status == 0."""
+    def _cb(_user, status):
+        try:
+            return 0 if barrier(int(status)) else 1
+        except Exception:  # a Python exception must not cross the C boundary
+            return 1
+    cb = RP_BARRIER_FN(_cb)
+    _check(load_library().rp_nvls_enable(ctx, min_gpus, cb, None), "rp_nvls_enable")
 
 
 def rp_schedule_static(ctx, rule, step, world):
@@ -405,6 +426,21 @@ class Context:
         records = [None] * dist.get_world_size(group)
         dist.all_gather_object(records, mine, group=group)
         self.peer_import(records)
+
+    def nvls_supported(self):
+        return rp_nvls_supported(self.handle)
+
+    def nvls_enable(self, min_gpus, group=None):
+        """Collective: create the multicast objects of every GPU subset of >= min_gpus GPUs
+        and route those cross-GPU groups through the in-switch (NVLS) P-Reduce. The
+        barrier is an all-gather of the ranks' status over torch.distributed."""
+        import torch.distributed as dist
+
+        def barrier(status):
+            out = [None] * dist.get_world_size(group)
+            dist.all_gather_object(out, status, group=group)
+            return all(v == 0 for v in out)
+        rp_nvls_enable(self.handle, min_gpus, barrier)
 
     def worker_stream(self, w):
         return rp_worker_stream(self.handle, w)

@@ -33,7 +33,7 @@ def _ceil_to(v, m):
 class LockstepRunner:
     def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
                  lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True,
-                 peer_group=None, section_length=1, momentum=None):
+                 peer_group=None, section_length=1, momentum=None, nvls=0):
         if mode not in ("static", "gd"):
             raise ValueError("mode must be 'static' or 'gd'")
         if mode == "static" and rule not in RULES:
@@ -64,6 +64,8 @@ class LockstepRunner:
             # map the peers' replicas + flag arrays (CUDA IPC records exchanged over
             # torch.distributed; the data path is the library's NVLink kernel)
             self.ctx.peer_setup(peer_group)
+            if nvls:   # groups spanning >= nvls GPUs reduce inside the NVSwitch (rp_nvls_enable)
+                self.ctx.nvls_enable(nvls, peer_group)
         self.t = 0
         if init:
             self.init_replicas()

@@ -93,3 +93,28 @@ def test_multi_gpu_async_shared_gg_replay(gpus, wpg, n, k, c_thres, steps, tmp_p
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, dict(wpg=wpg, n=n, k=k, c_thres=c_thres, steps=steps, tmp=str(tmp_path)),
          script="multi_gpu_async_worker.py")
+
+
+NVLS_CASES = [
+    # (gpus, spec): NVLS P-Reduce (rp_nvls_enable). kp = 2 groups are bit-exact
+    # (fp32 addition of two partials is commutative); kp >= 3 groups sum in the switch's order
+    # (reading R25) and are held to the north-star bound 1e-6 * max|x| (tol).
+    (2, dict(wpg=1, n=(1 << 20) + 3, k=2, mode="static", rule="shift_k", steps=20, nvls=2)),
+    (2, dict(wpg=2, n=100_003, k=3, mode="static", rule="shift_k", steps=12, nvls=2)),
+    (2, dict(wpg=4, n=100_003, k=3, mode="gd", steps=12, nvls=2)),
+    (2, dict(wpg=1, n=5, k=2, mode="static", rule="shift_k", steps=6, nvls=2)),
+    (2, dict(wpg=1, n=1, k=2, mode="static", rule="shift_k", steps=4, nvls=2)),
+    (2, dict(wpg=2, n=60_011, k=3, mode="static", rule="shift_k", steps=10, nvls=2, momentum=[0.9, 1e-4])),
+    (2, dict(wpg=1, n=N_R50, k=2, mode="gd", steps=4, sample=4099, nvls=2)),
+    (4, dict(wpg=1, n=200_003, k=3, mode="gd", steps=20, nvls=3, tol=1e-6)),
+    (4, dict(wpg=2, n=200_003, k=3, mode="static", rule="shift_k", steps=20, nvls=2, tol=1e-6)),
+    (4, dict(wpg=4, n=60_001, k=4, mode="static", rule="paper4", steps=8, nvls=3, tol=1e-6)),
+    (4, dict(wpg=8, n=30_011, k=3, mode="gd", steps=10, nvls=2, tol=1e-6)),
+]
+
+
+@pytest.mark.parametrize("gpus,spec", NVLS_CASES)
+def test_multi_gpu_nvls_parity(gpus, spec):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, **spec})
