@@ -22,6 +22,10 @@ import sys
 import threading
 import time
 
+# NCCL's version banner would go to stdout ahead of the JSON line (NCCL_DEBUG=VERSION/INFO)
+if not os.environ.get("RP_KEEP_NCCL_DEBUG"):
+    os.environ["NCCL_DEBUG"] = "WARN"
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -46,6 +50,11 @@ WORKLOADS = {
     "cfg4": dict(desc="configs[3]: 2 workers per B200 (16 on 8 GPUs), VGG-16-sized 138M fp32, k=3, static "
                       "SHIFT_K(2N,3)",
                  wpg=2, n=N_VGG, k=3, mode="static", rule="shift_k"),
+    "xall": dict(desc="diagnostic: 1 worker per B200, ResNet-50-sized, ONE group of all N GPUs every step "
+                      "(SHIFT_K(N,N)): the cross-GPU kernel's NVLink efficiency without lockstep skew",
+                 wpg=1, n=N_R50, k=64, mode="static", rule="shift_k"),
+    "xall_vgg": dict(desc="diagnostic: 1 worker per B200, VGG-16-sized, ONE group of all N GPUs every step",
+                     wpg=1, n=N_VGG, k=64, mode="static", rule="shift_k"),
     "cfg5": dict(desc="configs[4]: 2 workers per B200, VGG-16-sized, k=3, asynchronous GB+GD+filter (C_thres=4), "
                       "worker 0 slowed by --slow x T_c of device delay per step (P:1395)",
                  wpg=2, n=N_VGG, k=3, mode="async", rule=None),
@@ -245,6 +254,15 @@ def run_ours(args, wl):
                     "kernel_ms_per_launch": round(x_ms / max(1, nl), 4),
                     "algorithmic_nvlink_bytes_per_launch_per_gpu": int(x_b / max(1, nl)),
                     "hbm_achieved": round(ah, 1), "hbm_frac": round(ah / peaks["hbm_gbs"], 4)}
+        # the schedule may load GPUs unequally (e.g. SHIFT_K with 2 workers/GPU puts some GPUs
+        # in two cross-GPU groups per step): the GPU with the most NVLink bytes sets the pace
+        busy = max(per_rank, key=lambda r: r["tim"]["cross_bytes_nvlink"])
+        if busy["tim"]["cross_ms"] > 0:
+            ab = busy["tim"]["cross_bytes_nvlink"] / (busy["tim"]["cross_ms"] / 1e3) / 1e9
+            nvl_roof["busiest_gpu"] = {"achieved": round(ab, 1), "frac": round(ab / NVLINK_PEAK, 4),
+                                       "nvlink_bytes": int(busy["tim"]["cross_bytes_nvlink"]),
+                                       "share_of_all_nvlink_bytes": round(busy["tim"]["cross_bytes_nvlink"] /
+                                                                          max(1, x_b), 4)}
         if ah / peaks["hbm_gbs"] > a / NVLINK_PEAK:      # fused local work dominates: HBM-bound
             nvl_roof.update({"bound": "hbm", "achieved": round(ah, 1), "peak": peaks["hbm_gbs"],
                              "peak_source": peak_src, "frac": round(ah / peaks["hbm_gbs"], 4),
