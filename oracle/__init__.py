@@ -21,6 +21,9 @@ Modules and what pins them (tests/test_oracle_*.py, all ``-m "not gpu"``):
             pins: X·F^G closed form (fp64 library matmul), k=2 exact-halving
             identity, singleton = SGD within 1 ulp, mass conservation,
             idempotence, G = all = global mean, exact rational replay
+            bf16 replicas (reading R26): bf16_round pinned to hand-derived
+            IEEE ties (tests/golden/bf16_rne_ties.txt) and torch's RNE
+            conversion; update = fp32 update rounded once; half-ulp bound
   schedule  static rules PAPER4 and SHIFT_K
             pins: P:879 printed facts, fig:scheduler table, exhaustive
             disjointness / coverage / union-find connectivity

@@ -23,7 +23,7 @@ import numpy as np
 from rp_inputs import gen as xi_mod
 from . import schedule as sched_mod
 from .gg import GroupGenerator, ProtocolError, RandomGroupGenerator
-from .update import fused_group_update
+from .update import bf16_round, fused_group_update, fused_group_update_bf16
 
 F32 = np.float32
 
@@ -35,7 +35,7 @@ def init_replicas(n, n_params, lo=0, hi=None):
 def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
                  rule=None, k=None, nodes=None, m=None, c_thres=4, seed_gd=3,
                  lo=0, hi=None, X=None, first_step=1, gg=None, log=None, ii_nodes=0,
-                 section_length=1, momentum=None, V=None):
+                 section_length=1, momentum=None, V=None, dtype="f32"):
     """Simulate `steps` lockstep steps; returns (X, log).
 
     mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter; ii_nodes > 0
@@ -47,9 +47,17 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
     [lo, hi) restricts the simulated element range (elementwise method, so a
     slice is computed exactly as in the full run).
     log: list receiving (t, [groups]) per step, groups as sorted tuples.
+    dtype "bf16": bf16 replicas and gradients (the generator's fp32 values rounded to bf16),
+    fp32 arithmetic, bf16 result (reading R26, fused_group_update_bf16).
     """
     hi = n_params if hi is None else hi
     X = init_replicas(n, n_params, lo, hi) if X is None else X
+    if dtype == "bf16":
+        X = {w: bf16_round(X[w]) for w in range(n)}
+        if momentum is not None:
+            raise ValueError("bf16 replicas: plain SGD only (reading R26)")
+    elif dtype != "f32":
+        raise ValueError(dtype)
     wpg = workers_per_gpu or n
     log = [] if log is None else log
     if mode == "gd" and gg is None:
@@ -73,12 +81,13 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
         else:
             raise ValueError(mode)
         in_group = set(w for g in groups for w in g)
-        for g in groups:
+        singles = [(w,) for w in range(n) if w not in in_group]   # skip: SGD only
+        for g in [tuple(g) for g in groups] + singles:
             G = {w: xi_mod.grad(w, t, n_params, lo, hi) for w in g}
-            fused_group_update(X, G, g, lr, wpg, V=V, mu=mu, wd=wd)
-        for w in range(n):
-            if w not in in_group:           # skip: SGD only (singleton)
-                fused_group_update(X, {w: xi_mod.grad(w, t, n_params, lo, hi)}, (w,), lr, wpg, V=V, mu=mu, wd=wd)
+            if dtype == "bf16":
+                fused_group_update_bf16(X, {w: bf16_round(G[w]) for w in g}, g, lr, wpg)
+            else:
+                fused_group_update(X, G, g, lr, wpg, V=V, mu=mu, wd=wd)
         log.append((t, [tuple(g) for g in groups] + [(w,) for w in range(n) if w not in in_group]))
     return X, log
 

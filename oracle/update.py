@@ -20,6 +20,11 @@ NumPy float32 array operations are IEEE-754 binary32 round-to-nearest-even and
 NumPy never contracts a*b+c into an FMA, so each line below is one rounding.
 
 ``*_fp64`` variants are the fp64 shadow used by the invariant pins.
+
+bf16 replicas with fp32 reduction (reading R26): replicas and
+gradients are stored as bfloat16; every value is widened exactly to fp32, step 2 and the
+fold / divide run in fp32 exactly as above, and the mean is rounded ONCE to bf16
+(IEEE round-to-nearest-even) when it is written to the members.
 """
 import numpy as np
 
@@ -44,6 +49,16 @@ def momentum_sgd_fp32(x, g, v, lr, mu, wd):
     gp = np.asarray(g, dtype=F32) + F32(wd) * x
     v_new = F32(mu) * np.asarray(v, dtype=F32) + gp
     return x - F32(lr) * v_new, v_new
+
+
+def bf16_round(x):
+    """fp32 -> bfloat16, IEEE round-to-nearest-even on the 16 dropped mantissa bits; returned
+    as float32 holding the bf16 value (finite inputs; overflow rounds to inf as IEEE does).
+    bf16 = the upper 16 bits of a binary32: add 0x7FFF plus the lowest kept bit, truncate."""
+    b = np.ascontiguousarray(x, dtype=F32).view(np.uint32).astype(np.uint64)
+    keep_lsb = (b >> np.uint64(16)) & np.uint64(1)
+    r = ((b + np.uint64(0x7FFF) + keep_lsb) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(F32)
 
 
 def _fold_order(members, workers_per_gpu):
@@ -92,6 +107,19 @@ def fused_group_update(X, G, members, lr, workers_per_gpu=None, V=None, mu=0.0, 
     for m in members:
         X[m] = xbar.copy()
     return xbar
+
+
+def fused_group_update_bf16(X, G, members, lr, workers_per_gpu=None):
+    """fused_group_update for bf16 replicas (reading R26): X[m], G[m] hold bf16 values (as
+    float32 arrays, widening is exact); step 2 and step 4 in the pinned fp32 order; every
+    member receives bf16_round(xbar). Returns the bf16 mean."""
+    members = sorted(members)
+    ys = {m: sgd_fp32(X[m], G.get(m), lr) for m in members}
+    xbar = ys[members[0]] if len(members) == 1 else preduce_fp32(ys, members, workers_per_gpu)
+    out = bf16_round(xbar)
+    for m in members:
+        X[m] = out.copy()
+    return out
 
 
 def preduce_fp64(vectors):
