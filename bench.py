@@ -44,6 +44,9 @@ WORKLOADS = {
                         "Synchronization (§5.2, GPU = node): Head Workers across GPUs, the rest per GPU, "
                         "then whole-GPU groups",
                    wpg=8, n=N_R50, k=3, mode="gd", rule=None, inter_intra=True),
+    "cfg2bf16": dict(desc="configs[1] layout (8 workers per B200, ResNet-50-sized, k=3, GB+GD) with bf16 replicas "
+                          "and gradients, fp32 arithmetic, one rounding of the mean (SURVEY §8 f4, reading R26)",
+                     wpg=8, n=N_R50, k=3, mode="gd", rule=None, dtype="bf16"),
     "cfg3": dict(desc="configs[2]: 1 worker per B200 (8 workers on 8 GPUs), ResNet-50-sized, k=3, GB+GD, "
                       "concurrent disjoint groups over NVLink",
                  wpg=1, n=N_R50, k=3, mode="gd", rule=None),
@@ -188,7 +191,7 @@ def run_ours(args, wl):
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
                             rank=rank, device=local_rank, grad_mode="resident", flags=flags,
                             nodes=n_gpus if wl.get("inter_intra") else 0, peer_group=pg,
-                            nvls=args.nvls if n_gpus > 1 else 0)
+                            nvls=args.nvls if n_gpus > 1 else 0, dtype=wl.get("dtype", "f32"))
     for _ in range(args.warmup):
         runner.step()
     runner.synchronize()
@@ -285,7 +288,7 @@ def run_ours(args, wl):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": "f32",                         # arithmetic; storage in config.storage
         "data": "synthetic (counter-based xi generator; resident replicas + gradients)",
         "impl": "ours",
         "preduce_gbs": round((hbm_step + nvl_step) * args.steps / (ms / 1e3) / 1e9, 1),
@@ -294,6 +297,7 @@ def run_ours(args, wl):
                    "lr": 0.1, "hbm_bytes_per_step": int(hbm_step), "nvlink_bytes_per_step": int(nvl_step),
                    "cross_gpu_groups_per_step": sum(r["cross"] for r in per_rank) / args.steps,
                    "nvls_min_gpus": args.nvls if n_gpus > 1 else 0,
+                   "storage": wl.get("dtype", "f32"),
                    "parallelism": f"{n_gpus} ranks x {wpg} workers, disjoint groups",
                    "l2": ("inputs larger than L2" if hbm_step / n_gpus > L2_BYTES else
                           "working set fits in L2 (no flush): L2-resident number")},
@@ -458,10 +462,11 @@ def run_e2e(runner, args, torch, pg):
     result (the first 4 averaged parameters of every local worker). Max over ranks."""
     steps = max(1, min(args.steps, args.e2e_steps))
     n = runner.n
-    host_g = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in runner.local]
+    gdt = runner.G.dtype
+    host_g = [torch.empty(n, dtype=gdt, pin_memory=True) for _ in runner.local]
     for i, w in enumerate(runner.local):
         host_g[i].copy_(runner.g(w), non_blocking=False)
-    host_out = torch.empty((len(runner.local), 4), dtype=torch.float32, pin_memory=True)
+    host_out = torch.empty((len(runner.local), 4), dtype=runner.X.dtype, pin_memory=True)
     runner.synchronize()
     streams = {w: torch.cuda.ExternalStream(runner.streams[w]) for w in runner.local}
     barrier(pg)
@@ -479,8 +484,8 @@ def run_e2e(runner, args, torch, pg):
     dt = max_over_ranks(time.perf_counter() - t0, pg)
     return {"value": round(runner.world * steps / dt, 1) if dt > 0 else None,
             "unit": "worker-steps/s", "steps": steps,
-            "h2d_bytes_per_step": 4 * n * runner.world,
-            "d2h_bytes_per_step": 16 * runner.world,
+            "h2d_bytes_per_step": host_g[0].element_size() * n * runner.world,
+            "d2h_bytes_per_step": 4 * host_out.element_size() * runner.world,
             "timer": "host wall clock around the public-API steps (includes pinned h2d/d2h), max over ranks"}
 
 
@@ -505,12 +510,16 @@ def oracle_steps(wl, n_gpus, sample, steps):
     import numpy as np
     from oracle import schedule as S
     from oracle.gg import GroupGenerator
-    from oracle.update import fused_group_update
+    from oracle.update import bf16_round, fused_group_update, fused_group_update_bf16
     from rp_inputs import gen
 
     world = wl["wpg"] * n_gpus
     X = {w: gen.x0(w, wl["n"], 0, sample) for w in range(world)}
     G = {w: gen.grad(w, 1, wl["n"], 0, sample) for w in range(world)}
+    bf = wl.get("dtype") == "bf16"
+    if bf:
+        X = {w: bf16_round(v) for w, v in X.items()}
+        G = {w: bf16_round(v) for w, v in G.items()}
     k = min(wl["k"], world)
     gg = (GroupGenerator(world, k, c_thres=4, seed_gd=3, nodes=n_gpus if wl.get("inter_intra") else 0)
           if wl["mode"] in ("gd", "async") else None)
@@ -530,7 +539,10 @@ def oracle_steps(wl, n_gpus, sample, steps):
             covered = {w for g in groups for w in g}
             groups = groups + [(w,) for w in range(world) if w not in covered]
         for g in groups:
-            fused_group_update(X, {w: G[w] for w in g}, g, lr, wl["wpg"])
+            if bf:
+                fused_group_update_bf16(X, {w: G[w] for w in g}, g, lr, wl["wpg"])
+            else:
+                fused_group_update(X, {w: G[w] for w in g}, g, lr, wl["wpg"])
     return time.perf_counter() - t0
 
 

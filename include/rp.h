@@ -81,6 +81,13 @@ extern "C" {
                                    nodes, the rest node-local) and an Intra group (whole
                                    node); nodes = cfg.nodes, or n_gpus when 0           */
 
+/* Replica / gradient storage (reading R26). Arithmetic is fp32
+ * in the pinned order of reading R1 for both; bf16 widens exactly on load and rounds the mean
+ * once (IEEE round-to-nearest-even) on store. bf16 contexts: one GPU, plain SGD (no
+ * rp_step_momentum), workers bound with rp_bind_worker_bf16. */
+#define RP_DTYPE_F32 0
+#define RP_DTYPE_BF16 1
+
 #define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
 #define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */
 
@@ -96,7 +103,7 @@ typedef struct rp_config {
   int32_t nodes;           /* PAPER4 node count (world = nodes * m); 0 = n_gpus          */
   uint64_t seed_gd;        /* splitmix64 seed of the GD random partition (reading R8)    */
   int32_t flags;           /* RP_FLAG_*                                                  */
-  int32_t reserved0;
+  int32_t dtype;           /* RP_DTYPE_*: storage type of replicas and gradients (0 = fp32) */
   uint64_t job_id;         /* RP_FLAG_SHARED_GG: same nonzero value on every rank        */
   int32_t reserved[4];
 } rp_config;
@@ -164,6 +171,10 @@ int rp_finalize(rp_ctx* ctx);
  * process's GPU, 16-byte aligned, n_params fp32 each; w must belong to this
  * rank (w / wpg == rank). Errors: RP_EINVAL, RP_ENODEV. */
 int rp_bind_worker(rp_ctx* ctx, int32_t w, float* x_dev, const float* g_dev);
+/* The same for a cfg.dtype = RP_DTYPE_BF16 context: x and g are bfloat16 arrays (raw 16-bit
+ * patterns) of n_params elements, 16-byte aligned. rp_bind_worker on a bf16 context and
+ * rp_bind_worker_bf16 on an fp32 context fail with RP_EINVAL. */
+int rp_bind_worker_bf16(rp_ctx* ctx, int32_t w, uint16_t* x_dev, const uint16_t* g_dev);
 
 /* The CUDA stream (cudaStream_t as void*) on which worker w's work is
  * ordered. Producing w's gradient on this stream makes rp_preduce wait for
@@ -292,6 +303,9 @@ int rp_retire(rp_ctx* ctx, int32_t w);
  * staged step contributes y = x. Errors: RP_ESTATE (already staged),
  * RP_EINVAL (misaligned / no buffer). */
 int rp_step(rp_ctx* ctx, int32_t w, const float* grad_dev, float lr);
+/* rp_step for a bf16 context with a bf16 gradient (grad = NULL: the bound g). On a bf16
+ * context rp_step accepts only grad = NULL. Errors as rp_step, RP_EINVAL on an fp32 context. */
+int rp_step_bf16(rp_ctx* ctx, int32_t w, const uint16_t* grad_dev, float lr);
 
 /* rp_step with the paper's ResNet-50 optimizer ("Momentum optimizer is
  * used with momentum=0.9 and weight_decay=1e-4"; reading R24): inside the fused

@@ -95,7 +95,18 @@ std::string members_str(const rp_group& g, uint64_t mask_filter = ~0ull) {
 
 // Algorithmic HBM bytes per element of one member: x read + x write, g read if stepped,
 // v read + write with momentum.
-int64_t member_bytes(const rp::MemberUpdate& u) {
+// intra-GPU kernel variant for bf16 replicas (RP_PREDUCE_BF16, see preduce_tma.cu)
+int bf16_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RP_PREDUCE_BF16");
+    v = e && *e ? std::atoi(e) : 6;  // warp-specialized, 8 KB tiles (profiles/r01_ws_sweep.txt)
+  }
+  return v;
+}
+
+int64_t member_bytes(const rp::MemberUpdate& u, bool bf16 = false) {
+  if (bf16) return u.g ? 6 : 4;
   if (!u.g) return 8;
   return u.v ? 20 : 12;
 }
@@ -305,7 +316,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
       for (int i = 0; i < a.g.size; ++i) {
         t.x[nm] = c->w[a.g.members[i]].x;
         t.u[nm] = a.u[i];
-        bytes += member_bytes(a.u[i]) * c->cfg.n_params;
+        bytes += member_bytes(a.u[i], c->cfg.dtype == RP_DTYPE_BF16) * c->cfg.n_params;
         ++nm;
       }
       t.ngroups++;
@@ -322,7 +333,9 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
       CUDA_TRY(cudaEventRecord(e0, L.stream));
     }
     std::string err;
-    const int rc = rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
+    const int rc = c->cfg.dtype == RP_DTYPE_BF16
+                       ? rp::launch_preduce_tma(t, c->cfg.n_params, L.stream, &err, bf16_variant(), true)
+                       : rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
     if (rc != RP_OK) return fail(rc, err);
     if (timing) {
       CUDA_TRY(cudaEventRecord(e1, L.stream));
@@ -709,6 +722,9 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
   if (k.group_size < 1 || k.group_size > RP_MAX_GROUP || k.group_size > k.world)
     return fail(RP_EINVAL, "rp_init: group_size must be in [1, min(16, world)]");
   if (k.n_gpus < 0 || k.n_gpus > RP_MAX_GPUS) return fail(RP_EINVAL, "rp_init: n_gpus must be in [0, 8]");
+  if (k.dtype != RP_DTYPE_F32 && k.dtype != RP_DTYPE_BF16) return fail(RP_EINVAL, "rp_init: unknown dtype");
+  if (k.dtype == RP_DTYPE_BF16 && k.n_gpus > 1)
+    return fail(RP_EINVAL, "rp_init: bf16 replicas are single-GPU in this version (no cross-GPU bf16 kernel)");
   if (k.n_gpus > 0) {
     if (k.workers_per_gpu < 1 || k.n_gpus * k.workers_per_gpu != k.world)
       return fail(RP_EINVAL, "rp_init: world must equal n_gpus * workers_per_gpu");
@@ -949,8 +965,24 @@ int rp_finalize(rp_ctx* c) {
   return RP_OK;
 }
 
+namespace {
+int bind_worker(rp_ctx* c, int32_t w, float* x, const float* g);
+}
+
 int rp_bind_worker(rp_ctx* c, int32_t w, float* x, const float* g) {
   if (!c) return fail(RP_EINVAL, "null ctx");
+  if (c->cfg.dtype != RP_DTYPE_F32) return fail(RP_EINVAL, "rp_bind_worker: bf16 context (use rp_bind_worker_bf16)");
+  return bind_worker(c, w, x, g);
+}
+
+int rp_bind_worker_bf16(rp_ctx* c, int32_t w, uint16_t* x, const uint16_t* g) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (c->cfg.dtype != RP_DTYPE_BF16) return fail(RP_EINVAL, "rp_bind_worker_bf16: fp32 context");
+  return bind_worker(c, w, reinterpret_cast<float*>(x), reinterpret_cast<const float*>(g));
+}
+
+namespace {
+int bind_worker(rp_ctx* c, int32_t w, float* x, const float* g) {
   if (!c->has_gpu) return fail(RP_ENODEV, "rp_bind_worker: host-only context");
   if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "rp_bind_worker: worker not local to this rank");
   if (!x || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(g) & 15))
@@ -967,6 +999,7 @@ int rp_bind_worker(rp_ctx* c, int32_t w, float* x, const float* g) {
   c->w[w].bound = true;
   return RP_OK;
 }
+}  // namespace
 
 int rp_worker_stream(rp_ctx* c, int32_t w, void** out) {
   if (!c || !out) return fail(RP_EINVAL, "null argument");
@@ -1072,8 +1105,25 @@ int rp_retire(rp_ctx* c, int32_t w) {
   return rc;
 }
 
+namespace {
+int stage_step(rp_ctx* c, int32_t w, const float* grad, float lr);
+}
+
 int rp_step(rp_ctx* c, int32_t w, const float* grad, float lr) {
   if (!c) return fail(RP_EINVAL, "null ctx");
+  if (c->cfg.dtype != RP_DTYPE_F32 && grad)
+    return fail(RP_EINVAL, "rp_step: bf16 context takes a bf16 gradient (rp_step_bf16)");
+  return stage_step(c, w, grad, lr);
+}
+
+int rp_step_bf16(rp_ctx* c, int32_t w, const uint16_t* grad, float lr) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (c->cfg.dtype != RP_DTYPE_BF16) return fail(RP_EINVAL, "rp_step_bf16: fp32 context");
+  return stage_step(c, w, reinterpret_cast<const float*>(grad), lr);
+}
+
+namespace {
+int stage_step(rp_ctx* c, int32_t w, const float* grad, float lr) {
   if (!c->has_gpu) return fail(RP_ENODEV, "rp_step: host-only context");
   if (!worker_ok(c, w) || !c->w[w].local) return fail(RP_EINVAL, "rp_step: worker not local");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1087,10 +1137,12 @@ int rp_step(rp_ctx* c, int32_t w, const float* grad, float lr) {
   s.upd = rp::MemberUpdate{gp, nullptr, lr, 0.f, 0.f};
   return RP_OK;
 }
+}  // namespace
 
 int rp_step_momentum(rp_ctx* c, int32_t w, const float* grad, float lr, float momentum, float weight_decay,
                      float* v_dev) {
   if (!c) return fail(RP_EINVAL, "null ctx");
+  if (c->cfg.dtype != RP_DTYPE_F32) return fail(RP_EINVAL, "rp_step_momentum: fp32 replicas only");
   if (!v_dev || (reinterpret_cast<uintptr_t>(v_dev) & 15))
     return fail(RP_EINVAL, "rp_step_momentum: momentum buffer must be a non-null 16-byte aligned device pointer");
   const int rc = rp_step(c, w, grad, lr);

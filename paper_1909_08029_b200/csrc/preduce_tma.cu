@@ -4,8 +4,12 @@
 // one cp.async.bulk (completion on an mbarrier, S-stage pipeline), and the mean tile is
 // written ONCE to shared memory and pushed to all k member replicas by k bulk stores.
 // C persistent CTAs per SM; CTAs are shared out among the launch's groups by bytes.
-// Default path for plain SGD steps (variant 3, see launch_preduce_multi); momentum steps
-// and groups larger than 8 take the LDG kernel of preduce.cu.
+// Default path for plain SGD steps: the warp-specialized kernel (variant 5 for fp32, 6 for
+// bf16 replicas; one producer warp, eight consumer warps, full/empty mbarriers, no CTA-wide
+// barrier in the loop); groups of 9-16 members take the CTA-synchronous kernel; momentum
+// steps take the LDG kernel of preduce.cu. bf16 replicas (reading R26) use the same bulk
+// copies (16 bytes = 8 elements) with fp32 arithmetic and one rounding of the mean.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -64,7 +68,205 @@ __host__ __device__ constexpr size_t smem_bytes() {
 }
 
 // The CTAs [cta_begin[gi], cta_begin[gi+1]) own group gi; each takes tiles b, b+nb, ...
-template <int K, int T, int kStages>
+// fl(s / K) (reading R1). For K = 2^j the product s * 2^-j is exact-scaled and correctly
+// rounded exactly like the quotient (both are RNE of the same real number), so it is the
+// same bits at a fraction of the cost of the IEEE division sequence.
+template <int K>
+__device__ __forceinline__ float div_k(float s) {
+  if constexpr ((K & (K - 1)) == 0) return __fmul_rn(s, 1.0f / static_cast<float>(K));
+  else return __fdiv_rn(s, static_cast<float>(K));
+}
+
+// bf16 helpers (reading R26): widening is exact; narrowing is IEEE round-to-nearest-even
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t bf_pack(float lo, float hi) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+}
+
+// 16 bytes of bf16 (8 elements) of every member -> the rounded mean, packed
+template <int K>
+__device__ __forceinline__ uint4 mean8_bf16(const float4* stage, int s2k, int T, int e, const MemberUpdate (&up)[K]) {
+  float acc[8];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const uint4 xw = reinterpret_cast<const uint4*>(stage)[(s2k + 2 * m) * T + e];
+    const uint32_t xs[4] = {xw.x, xw.y, xw.z, xw.w};
+    uint32_t gs[4] = {0, 0, 0, 0};
+    if (up[m].g) {
+      const uint4 gw = reinterpret_cast<const uint4*>(stage)[(s2k + 2 * m + 1) * T + e];
+      gs[0] = gw.x; gs[1] = gw.y; gs[2] = gw.z; gs[3] = gw.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float y0 = bf_lo(xs[q]), y1 = bf_hi(xs[q]);
+      if (up[m].g) {
+        y0 = step_sgd(y0, bf_lo(gs[q]), up[m].lr);
+        y1 = step_sgd(y1, bf_hi(gs[q]), up[m].lr);
+      }
+      acc[2 * q] = m == 0 ? y0 : __fadd_rn(acc[2 * q], y0);
+      acc[2 * q + 1] = m == 0 ? y1 : __fadd_rn(acc[2 * q + 1], y1);
+    }
+  }
+  if (K > 1) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = div_k<K>(acc[j]);
+  }
+  return make_uint4(bf_pack(acc[0], acc[1]), bf_pack(acc[2], acc[3]), bf_pack(acc[4], acc[5]),
+                    bf_pack(acc[6], acc[7]));
+}
+
+// 16 bytes of fp32 (4 elements) of every member -> the mean
+template <int K>
+__device__ __forceinline__ float4 mean4_f32(const float4* stage, int s2k, int T, int e, const MemberUpdate (&up)[K]) {
+  float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float sx = 0.f, sy = 0.f, sz = 0.f, sw = 0.f;
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const float4 xv = stage[(s2k + 2 * m) * T + e];
+    const float4 gv = up[m].g ? stage[(s2k + 2 * m + 1) * T + e] : xv;
+    const float4 y = step4<false>(xv, gv, v0, up[m]);
+    sx = m == 0 ? y.x : __fadd_rn(sx, y.x);
+    sy = m == 0 ? y.y : __fadd_rn(sy, y.y);
+    sz = m == 0 ? y.z : __fadd_rn(sz, y.z);
+    sw = m == 0 ? y.w : __fadd_rn(sw, y.w);
+  }
+  if (K > 1) {
+    sx = div_k<K>(sx);
+    sy = div_k<K>(sy);
+    sz = div_k<K>(sz);
+    sw = div_k<K>(sw);
+  }
+  return make_float4(sx, sy, sz, sw);
+}
+
+// ragged tail element j (n mod 4, or n mod 8 for bf16), scalar, same order
+template <int K, bool BF>
+__device__ __forceinline__ void tail_elem(float* const (&x)[K], const MemberUpdate (&up)[K], int64_t j) {
+  float acc = 0.f;
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    float y;
+    if constexpr (BF) {
+      y = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x[m])[j]) << 16);
+      if (up[m].g)
+        y = step_sgd(y, __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(up[m].g)[j]) << 16),
+                     up[m].lr);
+    } else {
+      y = step1<false>(x[m][j], up[m], j);
+    }
+    acc = m == 0 ? y : __fadd_rn(acc, y);
+  }
+  if (K > 1) acc = div_k<K>(acc);
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    if constexpr (BF) reinterpret_cast<uint16_t*>(x[m])[j] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+    else x[m][j] = acc;
+  }
+}
+
+// ---- warp-specialized variant ------------------------------------------------------------
+// Warp 8 produces (one elected lane issues the 2K bulk loads of a tile into a free stage),
+// warps 0-7 consume: each owns T/8 float4 of every tile, computes its slice of the mean into
+// its own double-buffered output slice and bulk-stores it to the k members itself. Stages
+// are handed back through an `empty` mbarrier (8 arrivals); there is no CTA-wide barrier in
+// the loop, so a warp never waits for the slowest warp of its CTA.
+constexpr int kWsConsumers = 8;
+constexpr int kWsThreads = 32 * (kWsConsumers + 1);
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int K, int T, int kStages, bool BF>
+__device__ void group_ws(const MultiTask& t, int gi, int first, int64_t n4, int64_t n, float4* smem) {
+  static_assert(T % (32 * kWsConsumers) == 0, "each consumer lane owns whole float4 columns");
+  constexpr int kPerWarp = T / kWsConsumers;
+  const int64_t nb = t.cta_begin[gi + 1] - t.cta_begin[gi];
+  const int64_t b = static_cast<int64_t>(blockIdx.x) - t.cta_begin[gi];
+  const int64_t tiles = (n4 + T - 1) / T;
+  const int64_t ntl = tiles > b ? (tiles - b + nb - 1) / nb : 0;
+  float4* stage = smem;                         // [kStages][2K][T]
+  float4* out = stage + kStages * 2 * K * T;    // [2][T]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out + 2 * T);
+  uint64_t* empty = full + kStages;
+  MemberUpdate up[K];
+  float* x[K];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    x[m] = t.x[first + m];
+    up[m] = t.u[first + m];
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWsConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWsConsumers) {  // producer
+    if (lane == 0) {
+      for (int64_t it = 0; it < ntl; ++it) {
+        const int s = static_cast<int>(it % kStages);
+        if (it >= kStages) mbar_wait(&empty[s], static_cast<uint32_t>((it / kStages - 1) & 1));
+        const int64_t base = (b + it * nb) * T;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(T), n4 - base) * 16);
+        uint32_t total = 0;
+#pragma unroll
+        for (int m = 0; m < K; ++m) total += up[m].g ? 2 * bytes : bytes;
+        mbar_expect_tx(&full[s], total);
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+          bulk_load(stage + (s * 2 * K + 2 * m) * T, x[m] + 4 * base, bytes, &full[s]);
+          if (up[m].g) bulk_load(stage + (s * 2 * K + 2 * m + 1) * T, up[m].g + 4 * base, bytes, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int e0 = warp * kPerWarp;
+  for (int64_t it = 0; it < ntl; ++it) {
+    const int s = static_cast<int>(it % kStages);
+    const int ob = static_cast<int>(it & 1);
+    const int64_t base = (b + it * nb) * T;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(T), n4 - base));
+    if (lane == 0) bulk_wait_read1();  // this warp's stores of tile it-2 have read out[ob]
+    __syncwarp();
+    mbar_wait(&full[s], static_cast<uint32_t>((it / kStages) & 1));
+#pragma unroll
+    for (int j = 0; j < kPerWarp / 32; ++j) {
+      const int e = e0 + j * 32 + lane;
+      if (e < cnt) {
+        if constexpr (BF)
+          reinterpret_cast<uint4*>(out)[ob * T + e] = mean8_bf16<K>(stage, s * 2 * K, T, e, up);
+        else
+          out[ob * T + e] = mean4_f32<K>(stage, s * 2 * K, T, e, up);
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[s]);  // stage s read by this warp
+      const int mine = max(0, min(kPerWarp, cnt - e0));
+      if (mine > 0) {
+#pragma unroll
+        for (int m = 0; m < K; ++m)
+          bulk_store(x[m] + 4 * (base + e0), out + ob * T + e0, static_cast<uint32_t>(mine * 16));
+      }
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  constexpr int kPer = BF ? 8 : 4;
+  const int64_t rem = n - kPer * n4;
+  if (b == 0 && threadIdx.x < rem) tail_elem<K, BF>(x, up, kPer * n4 + threadIdx.x);
+}
+
+// n4 = number of 16-byte vectors per replica (n/4 fp32 or n/8 bf16); n = elements
+template <int K, int T, int kStages, bool BF>
 __device__ void group_tma(const MultiTask& t, int gi, int first, int64_t n4, int64_t n, float4* smem) {
   const int64_t nb = t.cta_begin[gi + 1] - t.cta_begin[gi];
   const int64_t b = static_cast<int64_t>(blockIdx.x) - t.cta_begin[gi];
@@ -108,7 +310,10 @@ __device__ void group_tma(const MultiTask& t, int gi, int first, int64_t n4, int
     if (threadIdx.x == 0) bulk_wait_read1();  // stores of tile it-2 have read out[ob]
     __syncthreads();
     mbar_wait(&bar[s], static_cast<uint32_t>((it / kStages) & 1));
-    for (int e = threadIdx.x; e < cnt; e += kTThreads) {
+    if constexpr (BF) {
+      for (int e = threadIdx.x; e < cnt; e += kTThreads)
+        reinterpret_cast<uint4*>(out)[ob * T + e] = mean8_bf16<K>(stage, s * 2 * K, T, e, up);
+    } else for (int e = threadIdx.x; e < cnt; e += kTThreads) {
       float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f);
       float yx[K], yy[K], yz[K], yw[K];
 #pragma unroll
@@ -148,8 +353,29 @@ __device__ void group_tma(const MultiTask& t, int gi, int first, int64_t n4, int
     }
   }
   if (threadIdx.x == 0) bulk_wait_all();
-  // ragged n mod 4 tail: first CTA of the group, scalar (pinned order as above)
-  const int64_t rem = n - 4 * n4;
+  // ragged tail (n mod 4, or n mod 8 for bf16): first CTA of the group, scalar, same order
+  constexpr int kPer = BF ? 8 : 4;
+  const int64_t rem = n - kPer * n4;
+  if constexpr (BF) {
+    if (b == 0 && threadIdx.x < rem) {
+      const int64_t j = kPer * n4 + threadIdx.x;
+      float acc = 0.f;
+#pragma unroll
+      for (int m = 0; m < K; ++m) {
+        const uint16_t* xm = reinterpret_cast<const uint16_t*>(x[m]);
+        float y = __uint_as_float(static_cast<uint32_t>(xm[j]) << 16);
+        if (up[m].g)
+          y = step_sgd(y, __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(up[m].g)[j]) << 16),
+                       up[m].lr);
+        acc = m == 0 ? y : __fadd_rn(acc, y);
+      }
+      if (K > 1) acc = __fdiv_rn(acc, static_cast<float>(K));
+      const uint16_t r = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+#pragma unroll
+      for (int m = 0; m < K; ++m) reinterpret_cast<uint16_t*>(x[m])[j] = r;
+    }
+    return;
+  }
   if (b == 0 && threadIdx.x < rem) {
     const int64_t j = 4 * n4 + threadIdx.x;
     float y[K];
@@ -164,12 +390,12 @@ __device__ void group_tma(const MultiTask& t, int gi, int first, int64_t n4, int
   }
 }
 
-template <int K, int KMAX, int T, int S>
+template <int K, int KMAX, int T, int S, bool BF>
 __device__ __forceinline__ void tma_if(const MultiTask& t, int gi, int first, int64_t n4, int64_t n, float4* smem) {
-  if constexpr (K <= KMAX) group_tma<K, T, S>(t, gi, first, n4, n, smem);
+  if constexpr (K <= KMAX) group_tma<K, T, S, BF>(t, gi, first, n4, n, smem);
 }
 
-template <int KMAX, int T, int S, int C>
+template <int KMAX, int T, int S, int C, bool BF>
 __global__ void __launch_bounds__(kTThreads, C) preduce_tma_kernel(const MultiTask t, const int64_t n4,
                                                                    const int64_t n) {
   extern __shared__ __align__(128) float4 tsmem[];
@@ -177,26 +403,116 @@ __global__ void __launch_bounds__(kTThreads, C) preduce_tma_kernel(const MultiTa
   while (gi + 1 < t.ngroups && static_cast<int>(blockIdx.x) >= t.cta_begin[gi + 1]) ++gi;
   const int first = t.group_first[gi];
   switch (t.group_k[gi]) {
-    case 1: tma_if<1, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 2: tma_if<2, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 3: tma_if<3, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 4: tma_if<4, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 5: tma_if<5, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 6: tma_if<6, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    case 7: tma_if<7, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
-    default: tma_if<8, KMAX, T, S>(t, gi, first, n4, n, tsmem); break;
+    case 1: tma_if<1, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 2: tma_if<2, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 3: tma_if<3, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 4: tma_if<4, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 5: tma_if<5, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 6: tma_if<6, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 7: tma_if<7, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 8: tma_if<8, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 9: tma_if<9, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 10: tma_if<10, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 11: tma_if<11, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 12: tma_if<12, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 13: tma_if<13, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 14: tma_if<14, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    case 15: tma_if<15, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+    default: tma_if<16, KMAX, T, S, BF>(t, gi, first, n4, n, tsmem); break;
+  }
+}
+
+template <int K, int KMAX, int T, int S, bool BF>
+__device__ __forceinline__ void ws_if(const MultiTask& t, int gi, int first, int64_t n4, int64_t n, float4* smem) {
+  if constexpr (K <= KMAX) group_ws<K, T, S, BF>(t, gi, first, n4, n, smem);
+}
+
+template <int KMAX, int T, int S, int C, bool BF>
+__global__ void __launch_bounds__(kWsThreads, C) preduce_ws_kernel(const MultiTask t, const int64_t n4,
+                                                                   const int64_t n) {
+  extern __shared__ __align__(128) float4 wsmem[];
+  int gi = 0;
+  while (gi + 1 < t.ngroups && static_cast<int>(blockIdx.x) >= t.cta_begin[gi + 1]) ++gi;
+  const int first = t.group_first[gi];
+  switch (t.group_k[gi]) {
+    case 1: ws_if<1, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 2: ws_if<2, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 3: ws_if<3, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 4: ws_if<4, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 5: ws_if<5, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 6: ws_if<6, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    case 7: ws_if<7, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
+    default: ws_if<8, KMAX, T, S, BF>(t, gi, first, n4, n, wsmem); break;
   }
 }
 
 int g_sms_tma = 0;
 
-template <int KMAX, int T, int S, int C>
+// CTAs of one launch shared out among its groups in proportion to their member counts
+void share_ctas(MultiTask& t, int64_t cap) {
+  int64_t kt = 0;
+  for (int gi = 0; gi < t.ngroups; ++gi) kt += t.group_k[gi];
+  int32_t acc = 0;
+  for (int gi = 0; gi < t.ngroups; ++gi) {
+    t.cta_begin[gi] = acc;
+    acc += static_cast<int32_t>(std::max<int64_t>(1, (cap * t.group_k[gi]) / kt));
+  }
+  t.cta_begin[t.ngroups] = acc;
+}
+
+int sms() {
+  if (g_sms_tma == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms_tma, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms_tma <= 0) g_sms_tma = 148;
+  }
+  return g_sms_tma;
+}
+
+template <int KMAX, int T, int S, int C, bool BF>
+int launch_ws(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
+  constexpr size_t smem = (static_cast<size_t>(S) * 2 * KMAX + 2) * T * sizeof(float4) + 2 * S * sizeof(uint64_t);
+  static_assert(smem * C <= 226 * 1024, "C CTAs must fit one SM");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(preduce_ws_kernel<KMAX, T, S, C, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess) {
+      *err = "preduce_ws: shared memory attribute";
+      return RP_ECUDA;
+    }
+    attr = true;
+  }
+  share_ctas(t, std::max<int64_t>(static_cast<int64_t>(sms()) * C, t.ngroups));
+  preduce_ws_kernel<KMAX, T, S, C, BF><<<t.cta_begin[t.ngroups], kWsThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("preduce_ws launch: ") + cudaGetErrorString(e);
+    return RP_ECUDA;
+  }
+  return RP_OK;
+}
+
+// warp-specialized variants: 5 = 4 KB tiles (2 CTAs/SM where they fit), 6 = 8 KB tiles
+template <bool BF>
+int launch_ws_variant(int variant, int kmax, MultiTask t, int64_t n, cudaStream_t s, std::string* err) {
+  if (variant == 6) {
+    if (kmax <= 3) return launch_ws<3, 512, 3, 1, BF>(t, n, s, err);
+    if (kmax <= 4) return launch_ws<4, 512, 2, 1, BF>(t, n, s, err);
+    return launch_ws<8, 256, 3, 1, BF>(t, n, s, err);
+  }
+  if (kmax <= 3) return launch_ws<3, 256, 4, 2, BF>(t, n, s, err);
+  if (kmax <= 4) return launch_ws<4, 256, 3, 2, BF>(t, n, s, err);
+  return launch_ws<8, 256, 3, 1, BF>(t, n, s, err);
+}
+
+template <int KMAX, int T, int S, int C, bool BF = false>
 int launch_tma(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
   static_assert(C == 1 || smem_bytes<KMAX, T, S>() * C <= 226 * 1024, "C CTAs must fit one SM");
   const size_t smem = smem_bytes<KMAX, T, S>();
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(preduce_tma_kernel<KMAX, T, S, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(preduce_tma_kernel<KMAX, T, S, C, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem)) != cudaSuccess) {
       *err = "preduce_tma: shared memory attribute";
       return RP_ECUDA;
@@ -218,7 +534,7 @@ int launch_tma(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     acc += static_cast<int32_t>(std::max<int64_t>(1, (cap * t.group_k[gi]) / kt));
   }
   t.cta_begin[t.ngroups] = acc;
-  preduce_tma_kernel<KMAX, T, S, C><<<acc, kTThreads, smem, stream>>>(t, n / 4, n);
+  preduce_tma_kernel<KMAX, T, S, C, BF><<<acc, kTThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("preduce_tma launch: ") + cudaGetErrorString(e);
@@ -230,7 +546,7 @@ int launch_tma(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
 }  // namespace
 
 // Returns RP_EINVAL (caller falls back to the LDG kernel) for shapes it does not cover.
-int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string* err, int variant) {
+int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string* err, int variant, bool bf16) {
   int kmax = 0;
   int nm = 0;
   for (int gi = 0; gi < t.ngroups; ++gi) {
@@ -239,8 +555,19 @@ int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string*
   }
   for (int i = 0; i < nm; ++i)
     if (t.u[i].v != nullptr) return RP_EINVAL;  // momentum: LDG kernel
-  if (kmax > 8 || n < 4) return RP_EINVAL;
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((variant == 5 || variant == 6) && kmax <= 8) {
+    return bf16 ? launch_ws_variant<true>(variant, kmax, t, n, s, err)
+                : launch_ws_variant<false>(variant, kmax, t, n, s, err);
+  }
+  if (bf16) {  // bf16 replicas (reading R26): the only intra-GPU kernel for them
+    if (kmax <= 3) return launch_tma<3, 256, 4, 2, true>(t, n, s, err);
+    if (kmax <= 4) return launch_tma<4, 128, 6, 2, true>(t, n, s, err);
+    if (kmax <= 8) return launch_tma<8, 128, 6, 1, true>(t, n, s, err);
+    return launch_tma<16, 64, 6, 1, true>(t, n, s, err);
+  }
+  if (kmax > 16 || n < 4) return RP_EINVAL;
+  if (kmax > 8) return launch_tma<16, 64, 6, 1>(t, n, s, err);
   // (KMAX, tile float4s T, stages S, CTAs per SM C) variants for the sweep in scripts/tma_local.sh
   if (kmax <= 4) {
     switch (variant) {

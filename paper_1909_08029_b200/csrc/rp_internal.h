@@ -98,7 +98,8 @@ struct MultiTask {
 // Fused SGD + P-Reduce of groups whose members all live on the current GPU.
 int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::string* err);
 // The same with a TMA bulk-copy pipeline; RP_EINVAL for shapes it does not cover.
-int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string* err, int variant);
+int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string* err, int variant,
+                       bool bf16 = false);
 // ---- cross-GPU parts (xgpu.cu) ----------------------------------------------------------
 constexpr int kMaxXParts = 8;    // cross-GPU groups one GPU takes part in, per launch
 constexpr int kMaxXLocal = 8;    // local members of one cross-GPU group

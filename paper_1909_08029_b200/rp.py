@@ -28,6 +28,8 @@ RP_FLAG_TIMING = 0x2
 RP_FLAG_SHARED_GG = 0x4
 RP_FLAG_RANDOM_GG = 0x8
 RP_FLAG_INTER_INTRA = 0x10
+RP_DTYPE_F32 = 0
+RP_DTYPE_BF16 = 1
 RP_SCHED_PAPER4 = 1
 RP_SCHED_SHIFT_K = 2
 RP_WAIT_DEVICE = -1
@@ -52,7 +54,7 @@ class rp_config(ctypes.Structure):
         ("nodes", ctypes.c_int32),
         ("seed_gd", ctypes.c_uint64),
         ("flags", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
         ("job_id", ctypes.c_uint64),
         ("reserved", ctypes.c_int32 * 4),
     ]
@@ -138,6 +140,7 @@ _SIGNATURES = {
     "rp_init": (ctypes.c_int, [ctypes.POINTER(rp_config), ctypes.POINTER(_CTX)]),
     "rp_finalize": (ctypes.c_int, [_CTX]),
     "rp_bind_worker": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, _P]),
+    "rp_bind_worker_bf16": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, _P]),
     "rp_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(_P)]),
     "rp_set_worker_stream": (ctypes.c_int, [_CTX, ctypes.c_int32, _P]),
     "rp_peer_export": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_peer_info)]),
@@ -154,6 +157,7 @@ _SIGNATURES = {
     "rp_gg_release": (ctypes.c_int, [_CTX, ctypes.c_int64]),
     "rp_retire": (ctypes.c_int, [_CTX, ctypes.c_int32]),
     "rp_step": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float]),
+    "rp_step_bf16": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float]),
     "rp_step_momentum": (ctypes.c_int, [_CTX, ctypes.c_int32, _P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                          _P]),
     "rp_preduce": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.POINTER(rp_group)]),
@@ -313,6 +317,14 @@ def rp_step(ctx, w, grad, lr):
     _check(load_library().rp_step(ctx, w, _ptr(grad), ctypes.c_float(lr)), "rp_step")
 
 
+def rp_step_bf16(ctx, w, grad, lr):
+    _check(load_library().rp_step_bf16(ctx, w, _ptr(grad), ctypes.c_float(lr)), "rp_step_bf16")
+
+
+def rp_bind_worker_bf16(ctx, w, x, g=None):
+    _check(load_library().rp_bind_worker_bf16(ctx, w, _ptr(x), _ptr(g)), "rp_bind_worker_bf16")
+
+
 def rp_step_momentum(ctx, w, grad, lr, momentum, weight_decay, v):
     _check(load_library().rp_step_momentum(ctx, w, _ptr(grad), ctypes.c_float(lr), ctypes.c_float(momentum),
                                            ctypes.c_float(weight_decay), _ptr(v)), "rp_step_momentum")
@@ -368,8 +380,12 @@ class Context:
     """Owns one rp_ctx. Methods map 1:1 onto the C calls."""
 
     def __init__(self, world, n_params, *, n_gpus=1, workers_per_gpu=None, rank=0, device=None,
-                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0, job_id=0):
+                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0, job_id=0, dtype="f32"):
+        if dtype not in ("f32", "bf16"):
+            raise ValueError("dtype must be 'f32' or 'bf16'")
         cfg = rp_config()
+        cfg.dtype = RP_DTYPE_BF16 if dtype == "bf16" else RP_DTYPE_F32
+        self.dtype = dtype
         cfg.world = world
         cfg.n_gpus = n_gpus
         cfg.n_params = n_params
@@ -410,7 +426,7 @@ class Context:
             pass
 
     def bind_worker(self, w, x, g=None):
-        rp_bind_worker(self.handle, w, x, g)
+        (rp_bind_worker_bf16 if self.dtype == "bf16" else rp_bind_worker)(self.handle, w, x, g)
 
     def peer_export(self):
         return rp_peer_export(self.handle)
@@ -479,7 +495,7 @@ class Context:
         rp_retire(self.handle, w)
 
     def step(self, w, grad=None, lr=0.1):
-        rp_step(self.handle, w, grad, lr)
+        (rp_step_bf16 if self.dtype == "bf16" else rp_step)(self.handle, w, grad, lr)
 
     def step_momentum(self, w, grad=None, lr=0.1, momentum=0.9, weight_decay=1e-4, v=None):
         rp_step_momentum(self.handle, w, grad, lr, momentum, weight_decay, v)

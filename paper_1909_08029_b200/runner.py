@@ -33,7 +33,7 @@ def _ceil_to(v, m):
 class LockstepRunner:
     def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
                  lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True,
-                 peer_group=None, section_length=1, momentum=None, nvls=0):
+                 peer_group=None, section_length=1, momentum=None, nvls=0, dtype="f32"):
         if mode not in ("static", "gd"):
             raise ValueError("mode must be 'static' or 'gd'")
         if mode == "static" and rule not in RULES:
@@ -47,13 +47,19 @@ class LockstepRunner:
         self.momentum = momentum                              # (mu, weight_decay)
         self.world, self.n = world, n_params
         self.n_gpus, self.peer_group = n_gpus, peer_group
+        self.dtype = dtype                                    # "bf16": bf16 replicas (reading R26)
         self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device,
-                           group_size=group_size, c_thres=c_thres, nodes=nodes, seed_gd=seed_gd, flags=flags)
+                           group_size=group_size, c_thres=c_thres, nodes=nodes, seed_gd=seed_gd, flags=flags,
+                           dtype=dtype)
         self.local = self.ctx.local_workers()
         self.ld = _ceil_to(n_params, 64)
         dev = torch.device("cuda", self.device)
-        self.X = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
-        self.G = torch.empty((len(self.local), self.ld), dtype=torch.float32, device=dev)
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.X = torch.empty((len(self.local), self.ld), dtype=tdt, device=dev)
+        self.G = torch.empty((len(self.local), self.ld), dtype=tdt, device=dev)
+        # fp32 staging of the generated inputs, one row per worker (each used on its own stream)
+        self._tmp = (torch.empty((len(self.local), n_params), dtype=torch.float32, device=dev)
+                     if dtype == "bf16" else None)
         self.V = (torch.zeros((len(self.local), self.ld), dtype=torch.float32, device=dev)
                   if momentum is not None else None)
         self.streams = {}
@@ -71,7 +77,7 @@ class LockstepRunner:
             self.init_replicas()
         if grad_mode == "resident":
             for w in self.local:
-                rp.fill_xi(self.g(w), n_params, SEED_G, w, 1, 0, self.streams[w])
+                self._fill(self.g(w), SEED_G, w, 1)
         self.synchronize()
 
     # -- memory ----------------------------------------------------------------------
@@ -87,9 +93,20 @@ class LockstepRunner:
     def v(self, w):
         return self.V[self._row(w), :self.n]
 
+    def _fill(self, dst, seed, w, t):
+        """Seeded synthetic input xi(seed, w, t) into dst on w's stream; bf16 destinations get
+        the fp32 values rounded to nearest-even (input preparation, like the oracle's)."""
+        if self.dtype == "f32":
+            rp.fill_xi(dst, self.n, seed, w, t, 0, self.streams[w])
+            return
+        tmp = self._tmp[self._row(w)]
+        rp.fill_xi(tmp, self.n, seed, w, t, 0, self.streams[w])
+        with torch.cuda.stream(torch.cuda.ExternalStream(self.streams[w], device=self.device)):
+            dst.copy_(tmp)
+
     def init_replicas(self):
         for w in self.local:
-            rp.fill_xi(self.x(w), self.n, SEED_X, w, 0, 0, self.streams[w])
+            self._fill(self.x(w), SEED_X, w, 0)
         self.t = 0
 
     def synchronize(self):
@@ -125,7 +142,7 @@ class LockstepRunner:
         for w in self.local:
             g = grads[w] if grads is not None else None
             if grads is None and self.grad_mode == "per_step":
-                rp.fill_xi(self.g(w), self.n, SEED_G, w, t, 0, self.streams[w])
+                self._fill(self.g(w), SEED_G, w, t)
             if self.momentum is not None:
                 self.ctx.step_momentum(w, g, self.lr, self.momentum[0], self.momentum[1], self.v(w))
             else:

@@ -21,7 +21,7 @@ def _compare(runner, X_oracle, lo=0, hi=None):
     worst = 0.0
     scale = 0.0
     for w in runner.local:
-        got = runner.x(w)[lo:hi].cpu().numpy()
+        got = runner.x(w)[lo:hi].float().cpu().numpy()   # bf16 -> fp32 widening is exact
         want = X_oracle[w]
         worst = max(worst, float(np.max(np.abs(got.astype(np.float64) - want))))
         scale = max(scale, float(np.max(np.abs(want))))
@@ -144,4 +144,55 @@ def test_section_length_bit_exact():
     X, olog = sim.run_lockstep(4, n, T, mode="static", rule="shift_k", k=2, section_length=3)
     assert [g for _, g in log] == [sorted(gs) for _, gs in olog]
     _compare(r, X)
+    r.close()
+
+
+# ---- more than 8 members on one GPU (TMA kernel KMAX = 16) -------------------------------
+
+def test_sixteen_member_group_fp32():
+    n, T = 70_003, 6
+    r = LockstepRunner(16, n, mode="static", rule="shift_k", group_size=16)
+    r.run(T)
+    r.synchronize()
+    X, _ = sim.run_lockstep(16, n, T, mode="static", rule="shift_k", k=16)
+    _compare(r, X)
+    r.close()
+
+
+# ---- bf16 replicas with fp32 reduction (reading R26): bit-exact ------------
+
+@pytest.mark.parametrize("world,k,mode,rule,n,T", [
+    (4, 2, "static", "shift_k", (1 << 16) + 5, 30),     # configs[0] shape, n mod 8 = 5
+    (8, 3, "gd", None, (1 << 18) + 3, 20),              # configs[1] shape (GB + GD)
+    (16, 16, "static", "shift_k", 50_001, 5),           # one 16-member group
+    (12, 5, "gd", None, 30_011, 8),                     # k = 5 groups + remainder groups
+])
+def test_bf16_replicas_bit_exact(world, k, mode, rule, n, T):
+    r = LockstepRunner(world, n, mode=mode, rule=rule, group_size=k, dtype="bf16")
+    log = r.run(T)
+    r.synchronize()
+    X, olog = sim.run_lockstep(world, n, T, mode=mode, rule=rule, k=k, dtype="bf16")
+    assert [g for _, g in log] == [sorted(gs) for _, gs in olog]
+    _compare(r, X)
+    r.close()
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 15, 17])
+def test_bf16_tiny_and_ragged(n):
+    r = LockstepRunner(4, n, mode="static", rule="shift_k", group_size=2, dtype="bf16")
+    r.run(5)
+    r.synchronize()
+    X, _ = sim.run_lockstep(4, n, 5, mode="static", rule="shift_k", k=2, dtype="bf16")
+    _compare(r, X)
+    r.close()
+
+
+def test_bf16_full_size_sampled():
+    T = 4
+    r = LockstepRunner(8, N_R50, mode="gd", group_size=3, c_thres=4, seed_gd=3, dtype="bf16")
+    r.run(T)
+    r.synchronize()
+    for lo, hi in [(0, 4096), (N_R50 // 2 - 2048, N_R50 // 2 + 2048), (N_R50 - 4099, N_R50)]:
+        X, _ = sim.run_lockstep(8, N_R50, T, mode="gd", k=3, c_thres=4, seed_gd=3, lo=lo, hi=hi, dtype="bf16")
+        _compare(r, X, lo, hi)
     r.close()

@@ -226,3 +226,16 @@ def test_inter_intra_async_interleavings_bit_exact(tmp_path):
     events = [json.loads(ln) for ln in open(trace)]
     from oracle import sim
     sim.replay_trace(events, n, 16, k=k, c_thres=3, seed_gd=4, ii_nodes=nodes)
+
+
+def test_bf16_context_rules():
+    # reading R26: bf16 replicas are single-GPU in this version; the dtype is validated up front
+    with rp.Context(4, 1024, n_gpus=0, group_size=2, dtype="bf16") as c:
+        assert c.dtype == "bf16"
+    with pytest.raises(rp.RPError) as e:
+        rp.Context(4, 1024, n_gpus=2, group_size=2, dtype="bf16")
+    assert e.value.status == rp.RP_EINVAL
+    cfg = rp.rp.rp_config(world=4, n_gpus=0, n_params=16, workers_per_gpu=4, group_size=2, dtype=7)
+    with pytest.raises(rp.RPError) as e:
+        rp.rp.rp_init(cfg)
+    assert e.value.status == rp.RP_EINVAL
