@@ -64,6 +64,7 @@ WORKLOADS = {
 }
 NVLINK_PEAK = 770.0   # GB/s per direction, measured peer copy (B200_PROFILING.md)
 NVLINK_NOMINAL = 900.0
+HBM_NOMINAL = 7700.0  # GB/s, B200 HGX HBM3e (B200_PROFILING.md)
 
 
 def measured_peaks():
@@ -231,9 +232,14 @@ def run_ours(args, wl):
     hbm_roof = None
     if loc_ms > 0:
         a = loc_b / (loc_ms / 1e3) / 1e9
-        hbm_roof = {"bound": "hbm", "kernel": "preduce_tma_kernel (fused SGD + P-Reduce, intra-GPU groups, TMA bulk copies)",
+        hbm_roof = {"bound": "hbm",
+                    "kernel": "preduce_dyn_kernel (fused SGD + P-Reduce, intra-GPU groups, TMA bulk copies, "
+                              "warp-specialized, dynamic tiles)",
                     "achieved": round(a, 1), "peak": peaks["hbm_gbs"], "peak_source": peak_src, "unit": "GB/s",
                     "frac": round(a / peaks["hbm_gbs"], 4),
+                    # the measured peak is a torch copy (1:1 read:write); this kernel streams 2:1
+                    # read:write, which the HBM serves faster, so frac can exceed 1
+                    "frac_of_nominal": round(a / HBM_NOMINAL, 4),
                     "traffic": traffic_from_profiles(args.workload, n_gpus),
                     "launches": sum(r["tim"]["local_launches"] for r in per_rank),
                     "kernel_ms_per_launch": round(loc_ms / max(1, sum(r["tim"]["local_launches"] for r in per_rank)), 4),
@@ -623,7 +629,12 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if args.workload is None:
-        args.workload = "cfg2"
+        # N = 1: configs[1] exactly. N > 1: the same layout (8 workers per B200, ResNet-50 size,
+        # k = 3, GB + GD) weak-scaled with the paper's architecture-aware GD (§5.2 Inter-Intra,
+        # GPU = node), which the paper proposes for nodes of 4-8 workers because random
+        # division across nodes congests the interconnect; plain GD over 8N
+        # workers stays available as --workload cfg2
+        args.workload = "cfg2" if args.gpus == 1 else "cfg2ii"
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl)

@@ -100,7 +100,7 @@ int bf16_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("RP_PREDUCE_BF16");
-    v = e && *e ? std::atoi(e) : 6;  // warp-specialized, 8 KB tiles (profiles/r01_ws_sweep.txt)
+    v = e && *e ? std::atoi(e) : 7;  // warp-specialized, dynamic tiles (profiles/r01_split/)
   }
   return v;
 }
@@ -148,6 +148,8 @@ struct rp_ctx {
   std::string shm_name;
   int64_t trace_local_n = 0;
   cudaStream_t comm = nullptr;      // asynchronous cross-GPU launches, in GG order
+  cudaStream_t aux = nullptr;       // lockstep: intra-GPU groups beside the step's cross-GPU launch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::set<int64_t> xready;         // cross GG groups whose local members all arrived
   std::set<int64_t> xlaunched;      // cross GG groups this GPU has launched
   rp_stats stats{};
@@ -258,7 +260,7 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // member after every member's arrival event; every member's stream is then
 // ordered after the kernel and records its own completion event.
 int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
-                 cudaStream_t stream);
+                 cudaStream_t stream, int max_ctas = 0);
 int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream);
 int pump_cross(rp_ctx* c);
 
@@ -293,19 +295,42 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   WorkerSlot& L = c->w[launcher];
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if (((all >> m) & 1) && m != launcher) CUDA_TRY(cudaStreamWaitEvent(L.stream, c->w[m].ev_arrive, 0));
-  // With cross-GPU groups in the batch, intra-GPU groups of <= 4 members ride in
-  // the same launch (their HBM work overlaps the NVLink transfers).
+  // With cross-GPU groups in the batch the intra-GPU groups run BESIDE them: the cross
+  // launch (NVLink-bound; grid capped at RP_XGPU_SPLIT CTAs, default 296 = every resident
+  // slot) is issued first, the intra-GPU launch (HBM-bound, dynamic-tile TMA kernel) runs on
+  // a second stream and its CTAs take SMs as they free up, drawing tiles at run time
+  // (RP_XGPU_SPLIT=0: the older mode, intra-GPU groups of <= 4 members fused into the cross
+  // launch as L items; sweep profiles/r01_split/).
+  static int split_ctas = -1;
+  if (split_ctas < 0) {
+    const char* v = std::getenv("RP_XGPU_SPLIT");
+    split_ctas = v && *v ? std::atoi(v) : 296;
+  }
+  // Only when the cross-GPU work is ONE part (e.g. the Head Workers' group of Inter-Intra,
+  // §5.2): with several parts the cross kernel needs every SM (measured, profiles/r01_split/).
+  // The decision is per GPU; the cross kernel's chunk geometry does not depend on it.
+  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux &&
+                     c->cfg.dtype == RP_DTYPE_F32;
   std::vector<int64_t> fused;
-  if (!cross.empty()) {
+  if (!cross.empty() && !split) {
     bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
     for (int64_t q : seqs) ok = ok && c->active.at(q).g.size <= rp::kMaxFusedK;
     if (ok) fused.swap(seqs);
+  }
+  cudaStream_t intra_stream = L.stream;
+  if (split) {
+    CUDA_TRY(cudaEventRecord(c->ev_fork, L.stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    intra_stream = c->aux;
+    const int rc = launch_cross(c, cross, {}, L.stream, split_ctas);
+    if (rc != RP_OK) return rc;
   }
   // One fused launch for all remaining intra-GPU groups (chunked at kMaxTasks
   // groups / kMaxTaskMembers members).
   size_t gi = 0;
   while (gi < seqs.size()) {
     rp::MultiTask t{};
+    if (split) t.reserve_sms = split_ctas;  // xgpu: at most one CTA per SM at first
     int nm = 0;
     int64_t bytes = 0;
     while (gi < seqs.size() && t.ngroups < rp::kMaxTasks) {
@@ -330,27 +355,30 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
       e0 = timing_event(c);
       e1 = timing_event(c);
       if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
-      CUDA_TRY(cudaEventRecord(e0, L.stream));
+      CUDA_TRY(cudaEventRecord(e0, intra_stream));
     }
     std::string err;
     const int rc = c->cfg.dtype == RP_DTYPE_BF16
-                       ? rp::launch_preduce_tma(t, c->cfg.n_params, L.stream, &err, bf16_variant(), true)
-                       : rp::launch_preduce_multi(t, c->cfg.n_params, L.stream, &err);
+                       ? rp::launch_preduce_tma(t, c->cfg.n_params, intra_stream, &err, bf16_variant(), true)
+                       : rp::launch_preduce_multi(t, c->cfg.n_params, intra_stream, &err);
     if (rc != RP_OK) return fail(rc, err);
     if (timing) {
-      CUDA_TRY(cudaEventRecord(e1, L.stream));
+      CUDA_TRY(cudaEventRecord(e1, intra_stream));
       c->timed.push_back({e0, e1, bytes, 0, false});
     }
     c->stats.kernel_launches++;
     c->stats.bytes_hbm += bytes;
   }
   // NVLS groups first, then the push kernel: every GPU issues its cross-GPU launches in
-  // the same order, so no launch waits on a peer's later launch
-  if (!nv.empty()) {
+  // the same order, so no launch waits on a peer's later launch (split: already issued)
+  if (split) {
+    CUDA_TRY(cudaEventRecord(c->ev_join, c->aux));
+    CUDA_TRY(cudaStreamWaitEvent(L.stream, c->ev_join, 0));
+  } else if (!nv.empty()) {
     const int rc = launch_nvls_groups(c, nv, L.stream);
     if (rc != RP_OK) return rc;
   }
-  if (!cross.empty()) {
+  if (!split && !cross.empty()) {
     const int rc = launch_cross(c, cross, fused, L.stream);
     if (rc != RP_OK) return rc;
   }
@@ -370,7 +398,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
 // This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch
 // (caller holds mu; members' arrival events already joined into `stream`).
 int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, int max_ctas) {
   if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
   if (static_cast<int>(seqs.size()) > rp::kMaxXParts)
     return fail(RP_EINVAL, "more than 8 cross-GPU groups on one GPU in one step");
@@ -380,6 +408,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
   T.my_gpu = c->cfg.rank;
   T.n = c->cfg.n_params;
   T.my_flags = c->flags;
+  T.max_ctas = max_ctas;
   for (size_t pi = 0; pi < seqs.size(); ++pi) {
     ActiveGroup& a = c->active.at(seqs[pi]);
     rp::XPart& p = T.part[pi];
@@ -782,9 +811,12 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       s.own_stream = true;
     }
     if (k.n_gpus > 1) {
-      if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess) {
+      if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess) {
         rp_finalize(c);
-        return cuda_fail(e, "rp_init: comm stream");
+        return cuda_fail(e, "rp_init: comm streams");
       }
       if (const char* pp = std::getenv("RP_XGPU_PROFILE")) c->prof_path = pp;
       if (wpg > RP_MAX_LOCAL) {
@@ -931,6 +963,12 @@ int rp_finalize(rp_ctx* c) {
       cudaStreamSynchronize(c->comm);
       cudaStreamDestroy(c->comm);
     }
+    if (c->aux) {
+      cudaStreamSynchronize(c->aux);
+      cudaStreamDestroy(c->aux);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     cudaDeviceSynchronize();
     rp::nvls_teardown(&c->nvls);

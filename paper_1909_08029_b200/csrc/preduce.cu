@@ -247,13 +247,14 @@ int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::strin
     const char* v = std::getenv("RP_PREDUCE_MINB");
     minb = v && *v ? std::atoi(v) : 0;
   }
-  // TMA bulk-copy pipeline (preduce_tma.cu) by default: the warp-specialized variant 5 won
-  // the sweeps (profiles/r01_tma_local_sweep.txt, profiles/r01_ws_sweep.txt); 1-4 are the
-  // CTA-synchronous TMA variants; RP_PREDUCE_TMA=0 selects this file's LDG/STG kernel.
+  // TMA bulk-copy pipeline (preduce_tma.cu) by default: the warp-specialized kernel with
+  // dynamic tile scheduling (variant 7) won the sweeps (+11 % over the static split of
+  // variant 5, profiles/r01_split/sweep_*.txt); 5/6 are the statically split warp-specialized
+  // variants, 1-4 the CTA-synchronous ones; RP_PREDUCE_TMA=0 selects this file's LDG/STG kernel.
   static int use_tma = -1;
   if (use_tma < 0) {
     const char* v = std::getenv("RP_PREDUCE_TMA");
-    use_tma = v && *v ? std::atoi(v) : 5;
+    use_tma = v && *v ? std::atoi(v) : 7;
   }
   if (use_tma > 0) {
     const int rc = launch_preduce_tma(t, n, stream, err, use_tma);

@@ -4,15 +4,19 @@
 // one cp.async.bulk (completion on an mbarrier, S-stage pipeline), and the mean tile is
 // written ONCE to shared memory and pushed to all k member replicas by k bulk stores.
 // C persistent CTAs per SM; CTAs are shared out among the launch's groups by bytes.
-// Default path for plain SGD steps: the warp-specialized kernel (variant 5 for fp32, 6 for
-// bf16 replicas; one producer warp, eight consumer warps, full/empty mbarriers, no CTA-wide
-// barrier in the loop); groups of 9-16 members take the CTA-synchronous kernel; momentum
-// steps take the LDG kernel of preduce.cu. bf16 replicas (reading R26) use the same bulk
+// Default path for plain SGD steps: the warp-specialized kernel with dynamic tile scheduling
+// (variant 7, fp32 and bf16; one producer warp, eight consumer warps, full/empty mbarriers,
+// no CTA-wide barrier in the loop, tiles of all groups drawn from one global counter);
+// variants 5/6 split the tiles statically; groups of 9-16 members take the CTA-synchronous
+// kernel; momentum steps take the LDG kernel of preduce.cu. bf16 replicas (reading R26) use the same bulk
 // copies (16 bytes = 8 elements) with fp32 arithmetic and one rounding of the mean.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "rp_internal.h"
@@ -446,6 +450,172 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_ws_kernel(const MultiTa
   }
 }
 
+// ---- warp-specialized kernel with dynamic tile scheduling (variant 7) --------------------
+// Same pipeline and arithmetic as group_ws, but tiles are handed out at run time from one
+// global counter over ALL groups of the launch (tile id -> group id % ngroups, tile
+// id / ngroups), so any CTA works on any group and a CTA that becomes resident late (another
+// kernel held its SM, e.g. the step's cross-GPU launch on a second stream) simply finds
+// fewer tiles left: no static split, no tail from unequal CTA start times. The producer
+// fetches its next tile id one tile ahead (atomicAdd latency hidden behind the bulk loads)
+// and passes it to the consumers in shared memory beside the stage (published by the
+// stage's mbarrier arrive, release/acquire at CTA scope). The last CTA to finish resets the
+// launch's counter pair, so the next launch that takes this ring slot finds zeros.
+constexpr int kDynSlots = 4096;
+
+template <int K, int T, bool BF>
+__device__ __forceinline__ void dyn_consume(const MultiTask& t, int g, int64_t base, int cnt, const float4* stage,
+                                            int s2, float4* out, int ob, int e0, int lane) {
+  constexpr int kPerWarp = T / kWsConsumers;
+  MemberUpdate up[K];
+  const int first = t.group_first[g];
+#pragma unroll
+  for (int m = 0; m < K; ++m) up[m] = t.u[first + m];
+#pragma unroll
+  for (int j = 0; j < kPerWarp / 32; ++j) {
+    const int e = e0 + j * 32 + lane;
+    if (e < cnt) {
+      if constexpr (BF)
+        reinterpret_cast<uint4*>(out)[ob * T + e] = mean8_bf16<K>(stage, s2, T, e, up);
+      else
+        out[ob * T + e] = mean4_f32<K>(stage, s2, T, e, up);
+    }
+  }
+}
+
+template <int K, int KMAX, int T, bool BF>
+__device__ __forceinline__ void dyn_consume_if(const MultiTask& t, int g, int64_t base, int cnt, const float4* stage,
+                                               int s2, float4* out, int ob, int e0, int lane) {
+  if constexpr (K <= KMAX) dyn_consume<K, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane);
+}
+
+template <int KMAX, int T, bool BF>
+__device__ __forceinline__ void dyn_tail(const MultiTask& t, int g, int64_t j) {
+  const int first = t.group_first[g];
+  switch (t.group_k[g]) {
+#define RP_DYN_TAIL(KK)                                                  \
+  case KK:                                                               \
+    if constexpr (KK <= KMAX) {                                          \
+      float* x[KK];                                                      \
+      MemberUpdate up[KK];                                               \
+      for (int m = 0; m < KK; ++m) {                                     \
+        x[m] = t.x[first + m];                                           \
+        up[m] = t.u[first + m];                                          \
+      }                                                                  \
+      tail_elem<KK, BF>(x, up, j);                                       \
+    }                                                                    \
+    break;
+    RP_DYN_TAIL(1) RP_DYN_TAIL(2) RP_DYN_TAIL(3) RP_DYN_TAIL(4) RP_DYN_TAIL(5) RP_DYN_TAIL(6) RP_DYN_TAIL(7)
+    RP_DYN_TAIL(8)
+#undef RP_DYN_TAIL
+    default: break;
+  }
+}
+
+template <int KMAX, int T, int S, int C, bool BF>
+__global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiTask t, const int64_t n4,
+                                                                    const int64_t n, int* ctr) {
+  static_assert(T % (32 * kWsConsumers) == 0, "each consumer lane owns whole float4 columns");
+  constexpr int kPerWarp = T / kWsConsumers;
+  extern __shared__ __align__(128) float4 dsmem[];
+  float4* stage = dsmem;                        // [S][2 KMAX][T]
+  float4* out = stage + S * 2 * KMAX * T;       // [2][T]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out + 2 * T);
+  uint64_t* empty = full + S;
+  volatile int64_t* tile_of = reinterpret_cast<volatile int64_t*>(empty + S);  // [S]
+  const int64_t tiles = (n4 + T - 1) / T;
+  const int64_t total = tiles * t.ngroups;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWsConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kWsConsumers) {  // producer
+    if (lane == 0) {
+      int64_t next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
+      for (int64_t it = 0;; ++it) {
+        const int s = static_cast<int>(it % S);
+        if (it >= S) mbar_wait(&empty[s], static_cast<uint32_t>((it / S - 1) & 1));
+        const int64_t id = next;
+        tile_of[s] = id;
+        if (id >= total) {
+          mbar_arrive(&full[s]);  // end marker: phase completes with no bytes
+          break;
+        }
+        next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
+        const int g = static_cast<int>(id % t.ngroups);
+        const int first = t.group_first[g], K = t.group_k[g];
+        const int64_t base = (id / t.ngroups) * T;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(T), n4 - base) * 16);
+        uint32_t tot = 0;
+        for (int m = 0; m < K; ++m) tot += t.u[first + m].g ? 2 * bytes : bytes;
+        mbar_expect_tx(&full[s], tot);
+        for (int m = 0; m < K; ++m) {
+          bulk_load(stage + (s * 2 * KMAX + 2 * m) * T, t.x[first + m] + 4 * base, bytes, &full[s]);
+          if (t.u[first + m].g)
+            bulk_load(stage + (s * 2 * KMAX + 2 * m + 1) * T, t.u[first + m].g + 4 * base, bytes, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int e0 = warp * kPerWarp;
+    for (int64_t it = 0;; ++it) {
+      const int s = static_cast<int>(it % S);
+      const int ob = static_cast<int>(it & 1);
+      if (lane == 0) bulk_wait_read1();  // this warp's stores of tile it-2 have read out[ob]
+      __syncwarp();
+      mbar_wait(&full[s], static_cast<uint32_t>((it / S) & 1));
+      const int64_t id = tile_of[s];
+      if (id >= total) break;
+      const int g = static_cast<int>(id % t.ngroups);
+      const int64_t base = (id / t.ngroups) * T;
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(T), n4 - base));
+      const int s2 = s * 2 * KMAX;
+      const int K = t.group_k[g];
+      switch (K) {
+        case 1: dyn_consume_if<1, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 2: dyn_consume_if<2, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 3: dyn_consume_if<3, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 4: dyn_consume_if<4, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 5: dyn_consume_if<5, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 6: dyn_consume_if<6, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        case 7: dyn_consume_if<7, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+        default: dyn_consume_if<8, KMAX, T, BF>(t, g, base, cnt, stage, s2, out, ob, e0, lane); break;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);  // stage s read by this warp
+        const int mine = max(0, min(kPerWarp, cnt - e0));
+        if (mine > 0) {
+          const int first = t.group_first[g];
+          for (int m = 0; m < K; ++m)
+            bulk_store(t.x[first + m] + 4 * (base + e0), out + ob * T + e0, static_cast<uint32_t>(mine * 16));
+        }
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  // ragged tail (n mod 4, or n mod 8 for bf16) of every group: CTA 0, scalar, same order
+  constexpr int kPer = BF ? 8 : 4;
+  const int64_t rem = n - kPer * n4;
+  if (blockIdx.x == 0 && threadIdx.x < rem)
+    for (int g = 0; g < t.ngroups; ++g) dyn_tail<KMAX, T, BF>(t, g, kPer * n4 + threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned long long*>(ctr) + 1, 1ull) == gridDim.x - 1) {
+      reinterpret_cast<unsigned long long*>(ctr)[0] = 0;  // every CTA has drawn its end marker
+      reinterpret_cast<unsigned long long*>(ctr)[1] = 0;
+    }
+  }
+}
+
 int g_sms_tma = 0;
 
 // CTAs of one launch shared out among its groups in proportion to their member counts
@@ -483,7 +653,10 @@ int launch_ws(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     }
     attr = true;
   }
-  share_ctas(t, std::max<int64_t>(static_cast<int64_t>(sms()) * C, t.ngroups));
+  // a concurrent cross-GPU launch holds t.reserve_sms SMs: every CTA of this grid is
+  // resident from the start on the others (persistent CTAs, static tile split)
+  const int64_t free_sms = std::max<int64_t>(1, sms() - std::max(0, t.reserve_sms));
+  share_ctas(t, std::max<int64_t>(free_sms * C, t.ngroups));
   preduce_ws_kernel<KMAX, T, S, C, BF><<<t.cta_begin[t.ngroups], kWsThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -491,6 +664,64 @@ int launch_ws(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     return RP_ECUDA;
   }
   return RP_OK;
+}
+
+// ring of per-launch counter pairs (next tile, CTAs done), one ring per device
+unsigned long long* dyn_counters(std::string* err) {
+  static std::mutex mu;
+  static unsigned long long* ring[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ring[dev]) {
+    if (cudaMalloc(&ring[dev], kDynSlots * 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(ring[dev], 0, kDynSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+      *err = "preduce_dyn: counter ring allocation failed";
+      ring[dev] = nullptr;
+      return nullptr;
+    }
+  }
+  return ring[dev];
+}
+
+template <int KMAX, int T, int S, int C, bool BF>
+int launch_dyn(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
+  constexpr size_t smem = (static_cast<size_t>(S) * 2 * KMAX + 2) * T * sizeof(float4) + 2 * S * sizeof(uint64_t) +
+                          S * sizeof(int64_t);
+  static_assert(smem * C <= 226 * 1024, "C CTAs must fit one SM");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(preduce_dyn_kernel<KMAX, T, S, C, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess) {
+      *err = "preduce_dyn: shared memory attribute";
+      return RP_ECUDA;
+    }
+    attr = true;
+  }
+  unsigned long long* ring = dyn_counters(err);
+  if (!ring) return RP_ECUDA;
+  static std::atomic<uint64_t> next_slot{0};
+  int* ctr = reinterpret_cast<int*>(ring + 2 * (next_slot.fetch_add(1) % kDynSlots));
+  const int grid = sms() * C;
+  preduce_dyn_kernel<KMAX, T, S, C, BF><<<grid, kWsThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n, ctr);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("preduce_dyn launch: ") + cudaGetErrorString(e);
+    return RP_ECUDA;
+  }
+  return RP_OK;
+}
+
+template <bool BF>
+int launch_dyn_variant(int kmax, MultiTask t, int64_t n, cudaStream_t s, std::string* err) {
+  // beside a cross-GPU launch (reserve_sms > 0): one stage less, so two CTAs still fit an
+  // SM next to a cross-kernel CTA (80 KB + 80 KB + 32 KB)
+  if (t.reserve_sms > 0 && kmax <= 3) return launch_dyn<3, 256, 3, 2, BF>(t, n, s, err);
+  if (t.reserve_sms > 0 && kmax <= 4) return launch_dyn<4, 256, 2, 2, BF>(t, n, s, err);
+  if (kmax <= 3) return launch_dyn<3, 256, 4, 2, BF>(t, n, s, err);
+  if (kmax <= 4) return launch_dyn<4, 256, 3, 2, BF>(t, n, s, err);
+  return launch_dyn<8, 256, 3, 1, BF>(t, n, s, err);
 }
 
 // warp-specialized variants: 5 = 4 KB tiles (2 CTAs/SM where they fit), 6 = 8 KB tiles
@@ -503,6 +734,12 @@ int launch_ws_variant(int variant, int kmax, MultiTask t, int64_t n, cudaStream_
   }
   if (kmax <= 3) return launch_ws<3, 256, 4, 2, BF>(t, n, s, err);
   if (kmax <= 4) return launch_ws<4, 256, 3, 2, BF>(t, n, s, err);
+  static int k8 = -1;  // RP_WS_K8: stages for 5..8 members (sweep)
+  if (k8 < 0) {
+    const char* v = std::getenv("RP_WS_K8");
+    k8 = v && *v ? std::atoi(v) : 3;
+  }
+  if (k8 == 2) return launch_ws<8, 256, 2, 1, BF>(t, n, s, err);
   return launch_ws<8, 256, 3, 1, BF>(t, n, s, err);
 }
 
@@ -556,6 +793,8 @@ int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string*
   for (int i = 0; i < nm; ++i)
     if (t.u[i].v != nullptr) return RP_EINVAL;  // momentum: LDG kernel
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((variant == 7 || t.reserve_sms > 0) && kmax <= 8)
+    return bf16 ? launch_dyn_variant<true>(kmax, t, n, s, err) : launch_dyn_variant<false>(kmax, t, n, s, err);
   if ((variant == 5 || variant == 6) && kmax <= 8) {
     return bf16 ? launch_ws_variant<true>(variant, kmax, t, n, s, err)
                 : launch_ws_variant<false>(variant, kmax, t, n, s, err);

@@ -93,6 +93,7 @@ struct MultiTask {
   float* x[kMaxTaskMembers];
   MemberUpdate u[kMaxTaskMembers];
   int32_t cta_begin[kMaxTasks + 1];
+  int32_t reserve_sms;  // SMs left to a concurrent cross-GPU launch (0 = use every SM)
 };
 
 // Fused SGD + P-Reduce of groups whose members all live on the current GPU.
@@ -156,6 +157,7 @@ struct XTask {
   int64_t total_items;
   int64_t chl, nchl;                       // L items: chunk (float4) and chunks per local group
   unsigned long long* my_flags;
+  int32_t max_ctas;                        // grid cap (0 = every resident CTA slot)
   XItemRecord* prof;                       // nullptr unless profiling; indexed by item
   int32_t nlocal;
   XLocalGroup lg[kMaxXLocalGroups];

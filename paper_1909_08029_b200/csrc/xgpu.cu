@@ -641,6 +641,9 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   }
   int64_t cap = static_cast<int64_t>(g_sms) * occ;  // all CTAs co-resident
   if (g_cps > 0) cap = std::min<int64_t>(cap, static_cast<int64_t>(g_sms) * g_cps);
+  // chunk geometry below depends on `cap` only, never on T.max_ctas: every GPU of a group
+  // must cut the same chunks (flags are per chunk), whatever grid its own launch gets
+  const int64_t grid_cap = T.max_ctas > 0 ? std::min<int64_t>(cap, T.max_ctas) : cap;
   if (g_min_chunk < 0) g_min_chunk = env_int("RP_XGPU_CHUNK_F4", static_cast<int>(kMinChunkF4));
   for (int pi = 0; pi < T.nparts; ++pi) {
     XPart& p = T.part[pi];
@@ -658,7 +661,7 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   T.nchl = std::max<int64_t>(1, (n4 + T.chl - 1) / T.chl);
   const int rc = item_list(T, cap, &T.items, &T.total_items, err);
   if (rc != RP_OK) return rc;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(cap, T.total_items)));
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(grid_cap, T.total_items)));
   xgpu_kernel<M, U, MOM, TMA><<<blocks, kXThreads, smem, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -28,11 +28,12 @@ def _free_port():
     return p
 
 
-def _run(nproc, spec, timeout=600, script="multi_gpu_worker.py"):
+def _run(nproc, spec, timeout=600, script="multi_gpu_worker.py", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", script), json.dumps(spec)]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                       env={**os.environ, **(env or {})})
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert p.stdout.count("OK") == nproc, p.stdout
 
@@ -118,3 +119,19 @@ def test_multi_gpu_nvls_parity(gpus, spec):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, {"sample": 0, "rule": None, **spec})
+
+
+@pytest.mark.parametrize("gpus,split,spec", [
+    # fused mode (intra-GPU groups as L items of the cross launch) and a capped cross grid
+    (2, "0", dict(wpg=4, n=50_007, k=3, mode="gd", steps=8, ii=True)),
+    (2, "0", dict(wpg=4, n=100_003, k=3, mode="gd", steps=12)),
+    (2, "37", dict(wpg=4, n=50_007, k=3, mode="gd", steps=8, ii=True)),
+    (4, "37", dict(wpg=8, n=30_011, k=3, mode="gd", steps=8, ii=True)),
+])
+def test_multi_gpu_split_modes(gpus, split, spec):
+    # RP_XGPU_SPLIT: a GPU whose step has ONE cross part runs its intra-GPU groups beside the
+    # cross launch (default); 0 = fused L items; a cap must not change the chunk geometry
+    # (peers with different caps must still agree on every chunk flag)
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, **spec}, env={"RP_XGPU_SPLIT": split})
