@@ -47,6 +47,9 @@ WORKLOADS = {
     "cfg2bf16": dict(desc="configs[1] layout (8 workers per B200, ResNet-50-sized, k=3, GB+GD) with bf16 replicas "
                           "and gradients, fp32 arithmetic, one rounding of the mean (SURVEY §8 f4, reading R26)",
                      wpg=8, n=N_R50, k=3, mode="gd", rule=None, dtype="bf16"),
+    "cfg2iibf16": dict(desc="cfg2ii (Inter-Intra, 8 workers per B200, ResNet-50-sized, k=3) with bf16 replicas and "
+                            "gradients: fp32 arithmetic, fp32 partials over NVLink, the mean rounded once to bf16",
+                       wpg=8, n=N_R50, k=3, mode="gd", rule=None, inter_intra=True, dtype="bf16"),
     "cfg3": dict(desc="configs[2]: 1 worker per B200 (8 workers on 8 GPUs), ResNet-50-sized, k=3, GB+GD, "
                       "concurrent disjoint groups over NVLink",
                  wpg=1, n=N_R50, k=3, mode="gd", rule=None),

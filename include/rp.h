@@ -83,8 +83,9 @@ extern "C" {
 
 /* Replica / gradient storage (reading R26). Arithmetic is fp32
  * in the pinned order of reading R1 for both; bf16 widens exactly on load and rounds the mean
- * once (IEEE round-to-nearest-even) on store. bf16 contexts: one GPU, plain SGD (no
- * rp_step_momentum), workers bound with rp_bind_worker_bf16. */
+ * once (IEEE round-to-nearest-even) on store. bf16 contexts: plain SGD (no
+ * rp_step_momentum), workers bound with rp_bind_worker_bf16; across GPUs the per-GPU partial
+ * sums travel as fp32 and the rounded mean as bf16; no NVLS (rp_nvls_enable: RP_EINVAL). */
 #define RP_DTYPE_F32 0
 #define RP_DTYPE_BF16 1
 

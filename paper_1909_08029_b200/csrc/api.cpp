@@ -309,10 +309,10 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   // Only when the cross-GPU work is ONE part (e.g. the Head Workers' group of Inter-Intra,
   // §5.2): with several parts the cross kernel needs every SM (measured, profiles/r01_split/).
   // The decision is per GPU; the cross kernel's chunk geometry does not depend on it.
-  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux &&
-                     c->cfg.dtype == RP_DTYPE_F32;
+  const bool bf16 = c->cfg.dtype == RP_DTYPE_BF16;
+  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux;
   std::vector<int64_t> fused;
-  if (!cross.empty() && !split) {
+  if (!cross.empty() && !split && !bf16) {  // bf16: intra-GPU groups keep their own launch
     bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
     for (int64_t q : seqs) ok = ok && c->active.at(q).g.size <= rp::kMaxFusedK;
     if (ok) fused.swap(seqs);
@@ -409,6 +409,8 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
   T.n = c->cfg.n_params;
   T.my_flags = c->flags;
   T.max_ctas = max_ctas;
+  T.bf16 = c->cfg.dtype == RP_DTYPE_BF16;
+  const int64_t esz = T.bf16 ? 2 : 4;  // bytes per replica element
   for (size_t pi = 0; pi < seqs.size(); ++pi) {
     ActiveGroup& a = c->active.at(seqs[pi]);
     rp::XPart& p = T.part[pi];
@@ -489,6 +491,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
   if (rc != RP_OK) return fail(rc, err);
   // algorithmic bytes of this GPU's parts: NVLink bytes this GPU stores into peers
   // (A: its partials of the other slices; B: its slice's means to every peer)
+  // (fp32 partials are staged and pushed as fp32; bf16 replicas move esz = 2 bytes per element)
   int64_t nvl = 0, hbm = 0;
   for (int pi = 0; pi < T.nparts; ++pi) {
     const rp::XPart& p = T.part[pi];
@@ -496,11 +499,11 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
     int64_t mine = 4 * (hi - lo);
     if (p.me == p.kp - 1) mine += p.rem;
     const int64_t others = T.n - mine;
-    nvl += 4 * (others + (p.kp - 1) * mine);
+    nvl += 4 * others + esz * (p.kp - 1) * mine;
     int64_t rd = 0;
-    for (int m = 0; m < p.m; ++m) rd += member_bytes(p.u[m]) - 4;  // reads (x, g, v) + v write
+    for (int m = 0; m < p.m; ++m) rd += member_bytes(p.u[m], T.bf16) - esz;  // reads (x, g, v) + v write
     // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
-    hbm += rd * T.n + 4 * (p.kp - 1) * mine + 4 * p.m * mine + 8 * (p.m - 1) * others;
+    hbm += rd * T.n + 4 * (p.kp - 1) * mine + esz * p.m * mine + 2 * esz * (p.m - 1) * others;
   }
   hbm += hbm_local;
   if (timing) {
@@ -742,6 +745,20 @@ const char* rp_strerror(int status) {
   }
 }
 
+namespace {
+// Stream of the intra-GPU launch that runs beside a cross-GPU launch. RP_AUX_PRIO: 0 = default
+// priority (default), 1 = higher than the cross launch's stream, -1 = lower (experiment knob).
+cudaError_t create_aux_stream(cudaStream_t* s) {
+  const char* v = std::getenv("RP_AUX_PRIO");
+  const int want = v && *v ? std::atoi(v) : 0;
+  if (want == 0) return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, want > 0 ? greatest : least);
+}
+}  // namespace
+
 int rp_init(const rp_config* cfg, rp_ctx** out) {
   if (!cfg || !out) return fail(RP_EINVAL, "rp_init: null argument");
   *out = nullptr;
@@ -752,8 +769,6 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
     return fail(RP_EINVAL, "rp_init: group_size must be in [1, min(16, world)]");
   if (k.n_gpus < 0 || k.n_gpus > RP_MAX_GPUS) return fail(RP_EINVAL, "rp_init: n_gpus must be in [0, 8]");
   if (k.dtype != RP_DTYPE_F32 && k.dtype != RP_DTYPE_BF16) return fail(RP_EINVAL, "rp_init: unknown dtype");
-  if (k.dtype == RP_DTYPE_BF16 && k.n_gpus > 1)
-    return fail(RP_EINVAL, "rp_init: bf16 replicas are single-GPU in this version (no cross-GPU bf16 kernel)");
   if (k.n_gpus > 0) {
     if (k.workers_per_gpu < 1 || k.n_gpus * k.workers_per_gpu != k.world)
       return fail(RP_EINVAL, "rp_init: world must equal n_gpus * workers_per_gpu");
@@ -812,7 +827,7 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
     }
     if (k.n_gpus > 1) {
       if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess ||
-          (e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = create_aux_stream(&c->aux)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess) {
         rp_finalize(c);
@@ -939,6 +954,7 @@ int rp_nvls_enable(rp_ctx* c, int32_t min_gpus, rp_barrier_fn barrier, void* use
   std::lock_guard<std::mutex> lk(c->mu);
   if (!c->peers_ready) return fail(RP_ESTATE, "rp_nvls_enable: call rp_peer_import first");
   if (c->nvls.min_gpus > 0) return fail(RP_ESTATE, "rp_nvls_enable: already enabled");
+  if (c->cfg.dtype != RP_DTYPE_F32) return fail(RP_EINVAL, "rp_nvls_enable: fp32 replicas only");
   int subsets = 0;
   for (uint32_t m = 1; m < (1u << c->cfg.n_gpus); ++m) subsets += __builtin_popcount(m) >= min_gpus;
   if (subsets > 64) return fail(RP_EINVAL, "rp_nvls_enable: more than 64 GPU subsets (P:1239 cache bound)");

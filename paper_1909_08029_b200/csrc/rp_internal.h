@@ -158,6 +158,7 @@ struct XTask {
   int64_t chl, nchl;                       // L items: chunk (float4) and chunks per local group
   unsigned long long* my_flags;
   int32_t max_ctas;                        // grid cap (0 = every resident CTA slot)
+  int32_t bf16;                            // replicas / gradients are bf16 (reading R26)
   XItemRecord* prof;                       // nullptr unless profiling; indexed by item
   int32_t nlocal;
   XLocalGroup lg[kMaxXLocalGroups];

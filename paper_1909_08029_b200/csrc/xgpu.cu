@@ -101,17 +101,84 @@ __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned 
   while (ld_acquire_sys(f) != tag) __nanosleep(32);
 }
 
+// ---- element access: fp32 replicas, or bf16 replicas with fp32 arithmetic (reading R26) ----
+// A "vector" is 4 consecutive elements: 16 bytes of fp32 or 8 bytes of bf16. Staged partials
+// are always fp32 (the fold runs in fp32); the mean is rounded once to bf16 when stored.
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t bf_rn(float v) {  // IEEE round-to-nearest-even (finite)
+  const uint32_t b = __float_as_uint(v);
+  return (b + 0x7fffu + ((b >> 16) & 1u)) >> 16;
+}
+template <bool BF>
+__device__ __forceinline__ float4 ldx4(const float* base, int64_t i) {
+  if constexpr (BF) {
+    uint32_t a, b;
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(a), "=r"(b)
+                 : "l"(reinterpret_cast<const uint16_t*>(base) + 4 * i));
+    return make_float4(bf_lo(a), bf_hi(a), bf_lo(b), bf_hi(b));
+  } else {
+    return ldv(base + 4 * i);
+  }
+}
+template <bool BF>
+__device__ __forceinline__ float4 ldg4(const float* base, int64_t i) {
+  if constexpr (BF) {
+    uint32_t a, b;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(a), "=r"(b)
+                 : "l"(reinterpret_cast<const uint16_t*>(base) + 4 * i));
+    return make_float4(bf_lo(a), bf_hi(a), bf_lo(b), bf_hi(b));
+  } else {
+    return ldg_nc(base + 4 * i);
+  }
+}
+__device__ __forceinline__ uint2 pack_bf4(float4 v) {
+  return make_uint2(bf_rn(v.x) | (bf_rn(v.y) << 16), bf_rn(v.z) | (bf_rn(v.w) << 16));
+}
+template <bool BF>
+__device__ __forceinline__ void stx4(float* base, int64_t i, float4 v) {
+  if constexpr (BF) {
+    const uint2 w = pack_bf4(v);
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(reinterpret_cast<uint16_t*>(base) + 4 * i), "r"(w.x),
+                 "r"(w.y)
+                 : "memory");
+  } else {
+    stv(base + 4 * i, v);
+  }
+}
+template <bool BF>
+__device__ __forceinline__ float ldx1(const float* base, int64_t j) {
+  if constexpr (BF) return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(base)[j]) << 16);
+  else return base[j];
+}
+template <bool BF>
+__device__ __forceinline__ void stx1(float* base, int64_t j, float v) {
+  if constexpr (BF) reinterpret_cast<uint16_t*>(base)[j] = static_cast<uint16_t>(bf_rn(v));
+  else base[j] = v;
+}
+template <bool MOM, bool BF>
+__device__ __forceinline__ float step1x(const float* x, const MemberUpdate& u, int64_t j) {
+  if constexpr (BF) {
+    const float xv = ldx1<true>(x, j);
+    return u.g == nullptr ? xv : step_sgd(xv, ldx1<true>(u.g, j), u.lr);
+  } else {
+    return step1<MOM>(x[j], u, j);
+  }
+}
+
 // Local partial of my p.m (<= M) members at float4 index i (left fold, ascending worker id),
 // with alg1 step 2 applied (and momentum buffers updated: each element's partial is
 // computed exactly once, in its A or B item).
-template <int M, bool MOM>
+template <int M, bool MOM, bool BF = false>
 __device__ __forceinline__ float4 local_partial4(const XPart& p, int64_t i) {
   float4 xv[M], gv[M], vv[MOM ? M : 1];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     if (m < p.m) {
-      xv[m] = ldv(p.x[m] + 4 * i);
-      if (p.u[m].g) gv[m] = ldg_nc(p.u[m].g + 4 * i);
+      xv[m] = ldx4<BF>(p.x[m], i);
+      if (p.u[m].g) gv[m] = ldg4<BF>(p.u[m].g, i);
       if constexpr (MOM)
         if (p.u[m].v) vv[m] = ldv(p.u[m].v + 4 * i);
     }
@@ -129,12 +196,12 @@ __device__ __forceinline__ float4 local_partial4(const XPart& p, int64_t i) {
   }
   return s;
 }
-template <int M, bool MOM>
+template <int M, bool MOM, bool BF = false>
 __device__ __forceinline__ float local_partial1(const XPart& p, int64_t j) {
-  float s = step1<MOM>(p.x[0][j], p.u[0], j);
+  float s = step1x<MOM, BF>(p.x[0], p.u[0], j);
 #pragma unroll
   for (int m = 1; m < M; ++m)
-    if (m < p.m) s = __fadd_rn(s, step1<MOM>(p.x[m][j], p.u[m], j));
+    if (m < p.m) s = __fadd_rn(s, step1x<MOM, BF>(p.x[m], p.u[m], j));
   return s;
 }
 
@@ -187,7 +254,7 @@ __device__ void item_A(const XPart& p, int o, int64_t c) {
   }
 }
 
-template <int M, int U, bool MOM>
+template <int M, int U, bool MOM, int KPM = kMaxXGpus>
 __device__ void item_B(const XPart& p, int64_t c) {
   const int o = p.me;
   const ChunkRange r = chunk_range(p, o, c);
@@ -200,20 +267,20 @@ __device__ void item_B(const XPart& p, int64_t c) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
       if (i < r.hi) {
         const float4 mine = local_partial4<M, MOM>(p, i);
-        float4 part[kMaxXGpus];
+        float4 part[KPM];
 #pragma unroll
-        for (int d = 0; d < kMaxXGpus; ++d)
+        for (int d = 0; d < KPM; ++d)
           if (d < p.kp && d != o) part[d] = ldv(stage + stage_off(p, d, i - slo));
         float4 s = o == 0 ? mine : part[0];
 #pragma unroll
-        for (int d = 1; d < kMaxXGpus; ++d)
+        for (int d = 1; d < KPM; ++d)
           if (d < p.kp) s = add4(s, d == o ? mine : part[d]);
         const float4 xbar = div4(s, kf);
 #pragma unroll
         for (int m = 0; m < M; ++m)
           if (m < p.m) stv(p.x[m] + 4 * i, xbar);
 #pragma unroll
-        for (int d = 0; d < kMaxXGpus; ++d)
+        for (int d = 0; d < KPM; ++d)
           if (d < p.kp && d != o) stv(p.xfirst[d] + 4 * i, xbar);  // NVLink store
       }
     }
@@ -247,7 +314,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
-template <int M, int U, bool MOM>
+template <int M, int U, bool MOM, bool BF = false>
 __device__ void item_A_tma(const XPart& p, int o, int64_t c, float4* smem) {
   const ChunkRange r = chunk_range(p, o, c);
   const int64_t slo = slice_lo(p, o);
@@ -261,7 +328,7 @@ __device__ void item_A_tma(const XPart& p, int o, int64_t c, float4* smem) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
-      if (i < r.hi) sb[u * kXThreads + threadIdx.x] = local_partial4<M, MOM>(p, i);
+      if (i < r.hi) sb[u * kXThreads + threadIdx.x] = local_partial4<M, MOM, BF>(p, i);
     }
     fence_async_smem();
     __syncthreads();
@@ -274,7 +341,7 @@ __device__ void item_A_tma(const XPart& p, int o, int64_t c, float4* smem) {
   }
   if (r.tail && threadIdx.x < p.rem) {
     const int64_t j = 4 * p.n4 + threadIdx.x;
-    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M, MOM>(p, j);
+    dst[stage_off(p, p.me, p.n4 - slo) + threadIdx.x] = local_partial1<M, MOM, BF>(p, j);
   }
   if (threadIdx.x == 0) {
     bulk_wait_all();
@@ -282,7 +349,7 @@ __device__ void item_A_tma(const XPart& p, int o, int64_t c, float4* smem) {
   }
 }
 
-template <int M, int U, bool MOM>
+template <int M, int U, bool MOM, int KPM = kMaxXGpus, bool BF = false>
 __device__ void item_B_tma(const XPart& p, int64_t c, float4* smem) {
   const int o = p.me;
   const ChunkRange r = chunk_range(p, o, c);
@@ -299,28 +366,41 @@ __device__ void item_B_tma(const XPart& p, int64_t c, float4* smem) {
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
       if (i < r.hi) {
-        const float4 mine = local_partial4<M, MOM>(p, i);
-        float4 part[kMaxXGpus];
+        const float4 mine = local_partial4<M, MOM, BF>(p, i);
+        float4 part[KPM];
 #pragma unroll
-        for (int d = 0; d < kMaxXGpus; ++d)
+        for (int d = 0; d < KPM; ++d)
           if (d < p.kp && d != o) part[d] = ldv(stage + stage_off(p, d, i - slo));
         float4 s = o == 0 ? mine : part[0];
 #pragma unroll
-        for (int d = 1; d < kMaxXGpus; ++d)
+        for (int d = 1; d < KPM; ++d)
           if (d < p.kp) s = add4(s, d == o ? mine : part[d]);
         const float4 xbar = div4(s, kf);
 #pragma unroll
         for (int m = 0; m < M; ++m)
-          if (m < p.m) stv(p.x[m] + 4 * i, xbar);
-        sb[u * kXThreads + threadIdx.x] = xbar;
+          if (m < p.m) stx4<BF>(p.x[m], i, xbar);
+        if constexpr (BF) {
+          reinterpret_cast<uint2*>(sb)[u * kXThreads + threadIdx.x] = pack_bf4(xbar);
+          // bulk copies move multiples of 16 bytes: an odd last bf16 vector goes by plain store
+          if (((r.hi - t0) & 1) && i == r.hi - 1 && r.hi - t0 <= kTile)
+            for (int d = 0; d < KPM; ++d)
+              if (d < p.kp && d != o) stx4<true>(p.xfirst[d], i, xbar);  // NVLink
+        } else {
+          sb[u * kXThreads + threadIdx.x] = xbar;
+        }
       }
     }
     fence_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
-      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTile), r.hi - t0) * 16);
+      const int64_t cnt = min(static_cast<int64_t>(kTile), r.hi - t0);
+      const uint32_t bytes = static_cast<uint32_t>(BF ? (cnt & ~1LL) * 8 : cnt * 16);
       for (int d = 0; d < p.kp; ++d)
-        if (d != o) bulk_store(p.xfirst[d] + 4 * t0, sb, bytes);  // NVLink
+        if (d != o) {
+          void* dst = BF ? static_cast<void*>(reinterpret_cast<uint16_t*>(p.xfirst[d]) + 4 * t0)
+                         : static_cast<void*>(p.xfirst[d] + 4 * t0);
+          if (bytes) bulk_store(dst, sb, bytes);  // NVLink
+        }
       bulk_commit();
     }
     buf ^= 1;
@@ -328,13 +408,13 @@ __device__ void item_B_tma(const XPart& p, int64_t c, float4* smem) {
   if (r.tail && threadIdx.x < p.rem) {
     const int64_t j = 4 * p.n4 + threadIdx.x;
     const int64_t so = p.n4 - slo;
-    const float mine = local_partial1<M, MOM>(p, j);
+    const float mine = local_partial1<M, MOM, BF>(p, j);
     float s = o == 0 ? mine : stage[stage_off(p, 0, so) + threadIdx.x];
     for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == o ? mine : stage[stage_off(p, d, so) + threadIdx.x]);
     const float xbar = __fdiv_rn(s, kf);
-    for (int m = 0; m < p.m; ++m) p.x[m][j] = xbar;
+    for (int m = 0; m < p.m; ++m) stx1<BF>(p.x[m], j, xbar);
     for (int d = 0; d < p.kp; ++d)
-      if (d != o) p.xfirst[d][j] = xbar;
+      if (d != o) stx1<BF>(p.xfirst[d], j, xbar);
   }
   if (threadIdx.x == 0) {
     bulk_wait_all();
@@ -342,7 +422,7 @@ __device__ void item_B_tma(const XPart& p, int64_t c, float4* smem) {
   }
 }
 
-template <int M, int U>
+template <int M, int U, bool BF = false>
 __device__ void item_C(const XPart& p, int o, int64_t c) {
   if (p.m == 1) return;  // the owner stored xbar straight into my only replica
   const ChunkRange r = chunk_range(p, o, c);
@@ -351,7 +431,7 @@ __device__ void item_C(const XPart& p, int o, int64_t c) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = t0 + u * kXThreads + threadIdx.x;
-      if (i < r.hi) v[u] = ldv(p.x[0] + 4 * i);
+      if (i < r.hi) v[u] = ldx4<BF>(p.x[0], i);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -359,14 +439,14 @@ __device__ void item_C(const XPart& p, int o, int64_t c) {
       if (i < r.hi) {
 #pragma unroll
         for (int m = 1; m < M; ++m)
-          if (m < p.m) stv(p.x[m] + 4 * i, v[u]);
+          if (m < p.m) stx4<BF>(p.x[m], i, v[u]);  // exact for bf16 (already rounded)
       }
     }
   }
   if (r.tail && threadIdx.x < p.rem) {
     const int64_t j = 4 * p.n4 + threadIdx.x;
-    const float v = p.x[0][j];
-    for (int m = 1; m < p.m; ++m) p.x[m][j] = v;
+    const float v = ldx1<BF>(p.x[0], j);
+    for (int m = 1; m < p.m; ++m) stx1<BF>(p.x[m], j, v);
   }
 }
 
@@ -445,8 +525,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // M bounds the local member count of every part (register budget).
-template <int M, int U, bool MOM, bool TMA>
-__global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
+template <int M, int U, bool MOM, bool TMA, int MINB = 2, int KPM = kMaxXGpus, bool BF = false>
+__global__ void __launch_bounds__(kXThreads, MINB) xgpu_kernel(const XTask T) {
+  static_assert(!BF || (TMA && !MOM), "bf16 replicas: TMA variants, plain SGD only");
   extern __shared__ float4 xsmem[];  // TMA: two tiles of kXThreads * U float4
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // READY: my staging is free for these groups (my previous kernel has finished)
@@ -466,7 +547,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
     if (T.prof && threadIdx.x == 0) ts = gtimer();
     if (region == 3) {
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_L<1, MOM>(T, t);
+      if constexpr (!BF) item_L<1, MOM>(T, t);  // bf16 launches carry no L items (launch_xgpu)
       if (T.prof) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -491,7 +572,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
       if constexpr (TMA)
-        item_A_tma<M, U, MOM>(p, o, c, xsmem);
+        item_A_tma<M, U, MOM, BF>(p, o, c, xsmem);
       else
         item_A<M, U, MOM>(p, o, c);
       __syncthreads();
@@ -506,9 +587,9 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
       if constexpr (TMA)
-        item_B_tma<M, U, MOM>(p, t, xsmem);
+        item_B_tma<M, U, MOM, KPM, BF>(p, t, xsmem);
       else
-        item_B<M, 1, MOM>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
+        item_B<M, 1, MOM, KPM>(p, t);  // B keeps M + kp - 1 loads per float4 in flight already
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
@@ -522,7 +603,7 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const XTask T) {
       if (threadIdx.x == 0) wait_flag(flag_at(T.my_flags, p.slot, p.gpu[o], kFlagB, c), p.tag);
       __syncthreads();
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      item_C<M, U>(p, o, c);
+      item_C<M, U, BF>(p, o, c);
     }
     __syncthreads();
     if (T.prof && threadIdx.x == 0) {
@@ -545,7 +626,7 @@ int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : def;
 }
-int g_u = -1, g_cps = -1, g_lag = -1, g_order = -1, g_tma = -1;
+int g_u = -1, g_cps = -1, g_lag = -1, g_order = -1, g_tma = -1, g_lean = -1;
 int64_t g_min_chunk = -1;
 
 // Host-built work-item order, cached per launch shape. Virtual time in units of a
@@ -623,12 +704,12 @@ int item_list(const XTask& T, int64_t ctas, const uint32_t** out, int64_t* count
 }
 
 
-template <int M, int U, bool MOM = false, bool TMA = false>
+template <int M, int U, bool MOM = false, bool TMA = false, int MINB = 2, int KPM = kMaxXGpus, bool BF = false>
 int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   static int occ = 0;
   const size_t smem = TMA ? 2 * sizeof(float4) * kXThreads * U : 0;
   if (occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U, MOM, TMA>, kXThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, U, MOM, TMA, MINB, KPM, BF>, kXThreads, smem) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
@@ -641,16 +722,17 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   }
   int64_t cap = static_cast<int64_t>(g_sms) * occ;  // all CTAs co-resident
   if (g_cps > 0) cap = std::min<int64_t>(cap, static_cast<int64_t>(g_sms) * g_cps);
-  // chunk geometry below depends on `cap` only, never on T.max_ctas: every GPU of a group
-  // must cut the same chunks (flags are per chunk), whatever grid its own launch gets
   const int64_t grid_cap = T.max_ctas > 0 ? std::min<int64_t>(cap, T.max_ctas) : cap;
+  // chunk geometry depends on the SM count only, never on this launch's grid or
+  // instantiation: every GPU of a group must cut the same chunks (flags are per chunk)
+  const int64_t geom = static_cast<int64_t>(g_sms) * 2;
   if (g_min_chunk < 0) g_min_chunk = env_int("RP_XGPU_CHUNK_F4", static_cast<int>(kMinChunkF4));
   for (int pi = 0; pi < T.nparts; ++pi) {
     XPart& p = T.part[pi];
     // chunk: about one A and one B item per resident CTA (each CTA pays the system fence
     // behind a flag about twice per group: measured best on 2 B200, profiles/r01_xgpu_*),
     // at least g_min_chunk float4, at most kMaxChunks chunks per slice
-    int64_t ch = std::max<int64_t>({(p.S4 + cap - 1) / cap, g_min_chunk, (p.S4 + kMaxChunks - 1) / kMaxChunks});
+    int64_t ch = std::max<int64_t>({(p.S4 + geom - 1) / geom, g_min_chunk, (p.S4 + kMaxChunks - 1) / kMaxChunks});
     p.CH = (ch + kTileF4 - 1) / kTileF4 * kTileF4;
     p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
   }
@@ -662,7 +744,7 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   const int rc = item_list(T, cap, &T.items, &T.total_items, err);
   if (rc != RP_OK) return rc;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(grid_cap, T.total_items)));
-  xgpu_kernel<M, U, MOM, TMA><<<blocks, kXThreads, smem, stream>>>(T);
+  xgpu_kernel<M, U, MOM, TMA, MINB, KPM, BF><<<blocks, kXThreads, smem, stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("xgpu kernel launch: ") + cudaGetErrorString(e);
@@ -733,6 +815,17 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
     g_lag = env_int("RP_XGPU_LAG", 0);
     g_order = env_int("RP_XGPU_ORDER", 0);
     g_tma = env_int("RP_XGPU_TMA", 1);
+    g_lean = env_int("RP_XGPU_LEAN", 0);
+  }
+  if (T.bf16) {  // bf16 replicas (reading R26): TMA pushes, plain SGD, no fused local groups
+    if (mom || T.nlocal > 0) {
+      *err = "xgpu: bf16 replicas take plain SGD and no fused local groups";
+      return RP_EINVAL;
+    }
+    if (mmax <= 1) return launch_m<1, 2, false, true, 2, kMaxXGpus, true>(T, s, err);
+    if (mmax <= 2) return launch_m<2, 2, false, true, 2, kMaxXGpus, true>(T, s, err);
+    if (mmax <= 4) return launch_m<4, 1, false, true, 2, kMaxXGpus, true>(T, s, err);
+    return launch_m<8, 1, false, true, 2, kMaxXGpus, true>(T, s, err);
   }
   if (mom) {  // momentum buffers: separate instantiations keep the plain path's registers
     if (g_tma > 0) {
@@ -746,6 +839,13 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
     if (mmax <= 4) return launch_m<4, 1, true>(T, s, err);
     return launch_m<8, 1, true>(T, s, err);
   }
+  // RP_XGPU_LEAN=1 (experiment, off by default: no gain measured, profiles/r01_split/
+  // sweep_4_lean.txt): beside an intra-GPU launch, a lean instantiation (<= 80 registers at
+  // 3 CTAs per SM) so the intra-GPU kernel's CTAs still fit on every SM next to it
+  int kpmax = 0;
+  for (int pi = 0; pi < T.nparts; ++pi) kpmax = std::max(kpmax, T.part[pi].kp);
+  if (T.max_ctas > 0 && g_tma > 0 && mmax <= 2 && kpmax <= 4 && g_lean != 0)
+    return mmax <= 1 ? launch_m<1, 1, false, true, 3, 4>(T, s, err) : launch_m<2, 1, false, true, 3, 4>(T, s, err);
   if (g_tma > 0) {  // default: TMA bulk stores for the NVLink pushes (+17-31 % on 2 B200,
                     // profiles/r01_xgpu_tma_sweep_2gpu.txt); RP_XGPU_TMA=0 selects peer STG.128
     if (mmax <= 1) return g_u >= 4 ? launch_m<1, 4, false, true>(T, s, err) : launch_m<1, 2, false, true>(T, s, err);

@@ -33,7 +33,8 @@ def main():
     mom = tuple(a.momentum) if getattr(a, "momentum", None) else None
     r = LockstepRunner(world, a.n, mode=a.mode, rule=a.rule, group_size=a.k, n_gpus=ngpu, rank=rank,
                        device=local_rank, nodes=nodes, flags=rp.RP_FLAG_INTER_INTRA if ii else 0, momentum=mom,
-                       section_length=getattr(a, "section_length", 1), nvls=getattr(a, "nvls", 0))
+                       section_length=getattr(a, "section_length", 1), nvls=getattr(a, "nvls", 0),
+                       dtype=getattr(a, "dtype", "f32"))
     log = r.run(a.steps)
     r.synchronize()
     slices = [(0, a.n)] if not a.sample else [(0, a.sample), (a.n // 2, a.n // 2 + a.sample),
@@ -43,9 +44,9 @@ def main():
         X, olog = sim.run_lockstep(world, a.n, a.steps, mode=a.mode, rule=a.rule, k=a.k, nodes=nodes,
                                    m=(world // nodes if nodes else None), workers_per_gpu=a.wpg, lo=lo, hi=hi,
                                    ii_nodes=ngpu if ii else 0, momentum=mom,
-                                   section_length=getattr(a, "section_length", 1))
+                                   section_length=getattr(a, "section_length", 1), dtype=getattr(a, "dtype", "f32"))
         for w in r.local:
-            got = r.x(w)[lo:hi].cpu().numpy()
+            got = r.x(w)[lo:hi].float().cpu().numpy()   # bf16 widens exactly
             if getattr(a, "tol", 0) and not np.array_equal(got.view(np.uint32), X[w].view(np.uint32)):
                 # NVLS with kp >= 3: the switch's summation order (reading R25) -> north-star bound
                 err = float(np.max(np.abs(got.astype(np.float64) - X[w])))

@@ -135,3 +135,24 @@ def test_multi_gpu_split_modes(gpus, split, spec):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, {"sample": 0, "rule": None, **spec}, env={"RP_XGPU_SPLIT": split})
+
+
+BF16_CASES = [
+    # bf16 replicas across GPUs (reading R26): fp32 partials over NVLink, the mean rounded once
+    # to bf16 and pushed as bf16; bit-exact vs the oracle's fused_group_update_bf16
+    (2, dict(wpg=1, n=(1 << 20) + 3, k=2, mode="static", rule="shift_k", steps=12)),
+    (2, dict(wpg=2, n=100_003, k=3, mode="static", rule="shift_k", steps=10)),
+    (2, dict(wpg=4, n=100_001, k=3, mode="gd", steps=10)),
+    (2, dict(wpg=4, n=50_007, k=3, mode="gd", steps=8, ii=True)),
+    (2, dict(wpg=1, n=5, k=2, mode="static", rule="shift_k", steps=6)),
+    (2, dict(wpg=1, n=4102, k=2, mode="static", rule="shift_k", steps=6)),   # odd bf16 vector count
+    (4, dict(wpg=2, n=200_003, k=3, mode="gd", steps=10)),
+    (4, dict(wpg=8, n=30_011, k=3, mode="gd", steps=8, ii=True)),
+]
+
+
+@pytest.mark.parametrize("gpus,spec", BF16_CASES)
+def test_multi_gpu_bf16_parity(gpus, spec):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, "dtype": "bf16", **spec})

@@ -229,12 +229,13 @@ def test_inter_intra_async_interleavings_bit_exact(tmp_path):
 
 
 def test_bf16_context_rules():
-    # reading R26: bf16 replicas are single-GPU in this version; the dtype is validated up front
+    # reading R26: the dtype is validated up front (bf16 multi-GPU contexts are accepted;
+    # without a device they fail with RP_ENODEV, not RP_EINVAL)
     with rp.Context(4, 1024, n_gpus=0, group_size=2, dtype="bf16") as c:
         assert c.dtype == "bf16"
     with pytest.raises(rp.RPError) as e:
         rp.Context(4, 1024, n_gpus=2, group_size=2, dtype="bf16")
-    assert e.value.status == rp.RP_EINVAL
+    assert e.value.status == rp.RP_ENODEV
     cfg = rp.rp.rp_config(world=4, n_gpus=0, n_params=16, workers_per_gpu=4, group_size=2, dtype=7)
     with pytest.raises(rp.RPError) as e:
         rp.rp.rp_init(cfg)
