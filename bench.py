@@ -196,8 +196,14 @@ def run_ours(args, wl):
                             rank=rank, device=local_rank, grad_mode="resident", flags=flags,
                             nodes=n_gpus if wl.get("inter_intra") else 0, peer_group=pg,
                             nvls=args.nvls if n_gpus > 1 else 0, dtype=wl.get("dtype", "f32"))
-    for _ in range(args.warmup):
-        runner.step()
+    # steps are issued by the library's native lockstep executor (rp_lockstep_run: the same
+    # public calls as runner.step(), from C++); --per-call drives them from Python instead
+    step_fn = runner.step if args.per_call else (lambda: runner.run_native(1))
+    if args.per_call:
+        for _ in range(args.warmup):
+            runner.step()
+    else:
+        runner.run_native(args.warmup)
     runner.synchronize()
     runner.ctx.timing_read()                              # drop warm-up launches
     s0 = torch.cuda.ExternalStream(runner.streams[runner.local[0]])   # every batch launches here
@@ -207,8 +213,11 @@ def run_ours(args, wl):
     with ClockSampler(local_rank) as clk:
         runner.synchronize()
         ev0.record(s0)
-        for _ in range(args.steps):
-            runner.step()
+        if args.per_call:
+            for _ in range(args.steps):
+                runner.step()
+        else:
+            runner.run_native(args.steps)
         ev1.record(s0)
         runner.synchronize()
     barrier(pg)
@@ -220,7 +229,7 @@ def run_ours(args, wl):
                        "hbm": st1["bytes_hbm"] - st0["bytes_hbm"],
                        "nvl": st1["bytes_nvlink"] - st0["bytes_nvlink"],
                        "cross": st1["cross_gpu_groups"] - st0["cross_gpu_groups"]}, pg)
-    e2e = run_e2e(runner, args, torch, pg)
+    e2e = run_e2e(runner, args, torch, pg, step_fn)
     runner.close()
     if rank != 0:
         return
@@ -303,6 +312,7 @@ def run_ours(args, wl):
         "preduce_gbs": round((hbm_step + nvl_step) * args.steps / (ms / 1e3) / 1e9, 1),
         "config": {"workload": args.workload, "desc": wl["desc"], "world": world, "workers_per_gpu": wpg,
                    "n_params": n, "group_size": k, "schedule": wl["rule"] or "GB+GD (lockstep, ascending requests)",
+                   "driver": "per-call API from Python" if args.per_call else "rp_lockstep_run (native executor)",
                    "lr": 0.1, "hbm_bytes_per_step": int(hbm_step), "nvlink_bytes_per_step": int(nvl_step),
                    "cross_gpu_groups_per_step": sum(r["cross"] for r in per_rank) / args.steps,
                    "nvls_min_gpus": args.nvls if n_gpus > 1 else 0,
@@ -465,7 +475,7 @@ def run_nccl_ar(args, wl):
             flush=True)
 
 
-def run_e2e(runner, args, torch, pg):
+def run_e2e(runner, args, torch, pg, step_fn):
     """Same metric through the public API with host buffers: per step, h2d of every local worker's
     gradient from pinned host memory, the lockstep step, and a blocking d2h read of the step's
     result (the first 4 averaged parameters of every local worker). Max over ranks."""
@@ -484,7 +494,7 @@ def run_e2e(runner, args, torch, pg):
         for i, w in enumerate(runner.local):
             with torch.cuda.stream(streams[w]):
                 runner.g(w).copy_(host_g[i], non_blocking=True)
-        runner.step()
+        step_fn()
         for i, w in enumerate(runner.local):
             with torch.cuda.stream(streams[w]):
                 host_out[i].copy_(runner.x(w)[:4], non_blocking=True)
@@ -620,6 +630,8 @@ def main():
     ap.add_argument("--nvls", type=int, default=0,
                     help="N>1: cross-GPU groups spanning >= this many GPUs reduce inside the NVSwitch (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-call", action="store_true",
+                    help="drive each lockstep step from Python through the per-call API instead of rp_lockstep_run")
     ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
     ap.add_argument("--tc-us", type=float, default=2000.0, help="cfg5: synthetic compute time per step")
     ap.add_argument("--window", type=float, default=3.0, help="cfg5: measured wall-clock window (s)")

@@ -91,6 +91,7 @@ extern "C" {
 
 #define RP_SCHED_PAPER4 1       /* fig:scheduler 4-phase rule, P:883-923 (reading R4)  */
 #define RP_SCHED_SHIFT_K 2      /* cyclic fixed-size-k rule (reading R4)    */
+#define RP_SCHED_GG (-1)        /* rp_lockstep_run: the Group Generator (GB + GD, §5)   */
 
 typedef struct rp_config {
   int32_t world;           /* n workers, 1..RP_MAX_WORLD                                 */
@@ -375,6 +376,22 @@ int rp_compute_delay(void* stream, int64_t ns);
  * device memory. Errors: RP_EINVAL, RP_ECUDA. */
 int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                void* stream);
+
+/* Native lockstep executor (alg1, for every local worker of this rank): runs
+ * `steps` iterations t = t0, t0 + 1, ... (t0 >= 1) exactly as the per-call sequence
+ *   rp_step(w, NULL, lr) for every local w;
+ *   step 3: t % section_length != 0 -> singleton group {w} with seq
+ *           -(1 + t*world + w) (SGD only); rule RP_SCHED_PAPER4 / RP_SCHED_SHIFT_K ->
+ *           rp_schedule_static_worker(rule, t, w); rule RP_SCHED_GG -> rp_group_generate_many
+ *           over ALL world workers in ascending order (the replicated GG stays identical on
+ *           every rank);
+ *   rp_batch_begin; rp_preduce(w, its group) for every local w; rp_batch_end;
+ *   rp_barrier_free_wait(w, RP_WAIT_DEVICE) for every local w; rp_gg_release of every GG
+ *   group of the step with no local member (ascending seq).
+ * Every rank of a multi-GPU job calls it with the same arguments. Plain SGD with the bound
+ * gradients (fp32 or bf16 contexts); momentum steps use the per-call API. Returns the first
+ * failing call's status (RP_EINVAL for a bad rule / t0 / steps / section_length). */
+int rp_lockstep_run(rp_ctx* ctx, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length);
 
 #ifdef __cplusplus
 }

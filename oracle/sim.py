@@ -35,7 +35,7 @@ def init_replicas(n, n_params, lo=0, hi=None):
 def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
                  rule=None, k=None, nodes=None, m=None, c_thres=4, seed_gd=3,
                  lo=0, hi=None, X=None, first_step=1, gg=None, log=None, ii_nodes=0,
-                 section_length=1, momentum=None, V=None, dtype="f32"):
+                 section_length=1, momentum=None, V=None, dtype="f32", grad_step=None):
     """Simulate `steps` lockstep steps; returns (X, log).
 
     mode: "static" (rule "paper4" or "shift_k") or "gd" (GB + GD + filter; ii_nodes > 0
@@ -49,6 +49,8 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
     log: list receiving (t, [groups]) per step, groups as sorted tuples.
     dtype "bf16": bf16 replicas and gradients (the generator's fp32 values rounded to bf16),
     fp32 arithmetic, bf16 result (reading R26, fused_group_update_bf16).
+    grad_step: None draws g_w^t = xi(2, w, t) every step; an integer T keeps g_w^T for every
+    step (the resident-gradient harness of the bench and of rp_lockstep_run).
     """
     hi = n_params if hi is None else hi
     X = init_replicas(n, n_params, lo, hi) if X is None else X
@@ -83,7 +85,7 @@ def run_lockstep(n, n_params, steps, *, mode, lr=0.1, workers_per_gpu=None,
         in_group = set(w for g in groups for w in g)
         singles = [(w,) for w in range(n) if w not in in_group]   # skip: SGD only
         for g in [tuple(g) for g in groups] + singles:
-            G = {w: xi_mod.grad(w, t, n_params, lo, hi) for w in g}
+            G = {w: xi_mod.grad(w, t if grad_step is None else grad_step, n_params, lo, hi) for w in g}
             if dtype == "bf16":
                 fused_group_update_bf16(X, {w: bf16_round(G[w]) for w in g}, g, lr, wpg)
             else:

@@ -309,8 +309,14 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   // Only when the cross-GPU work is ONE part (e.g. the Head Workers' group of Inter-Intra,
   // §5.2): with several parts the cross kernel needs every SM (measured, profiles/r01_split/).
   // The decision is per GPU; the cross kernel's chunk geometry does not depend on it.
+  // ... and only when the intra-GPU work clearly dominates the step (at least twice the cross
+  // part's local members): a lone intra-GPU singleton beside a cross part (cfg 4) is faster fused
   const bool bf16 = c->cfg.dtype == RP_DTYPE_BF16;
-  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux;
+  int intra_members = 0, cross_members = 0;
+  for (int64_t q : seqs) intra_members += c->active.at(q).g.size;
+  for (int64_t q : cross) cross_members += __builtin_popcountll(c->active.at(q).local_mask);
+  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux &&
+                     intra_members >= 2 * cross_members;
   std::vector<int64_t> fused;
   if (!cross.empty() && !split && !bf16) {  // bf16: intra-GPU groups keep their own launch
     bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
@@ -1429,3 +1435,79 @@ int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uin
 }
 
 }  // extern "C"
+
+// Native lockstep executor: the LockstepRunner's step loop (runner.py) composed from the public
+// calls above, so a lockstep step costs no per-call host overhead beyond C++.
+int rp_lockstep_run(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "rp_lockstep_run: host-only context");
+  if (steps < 0 || t0 < 1 || section_length < 1 ||
+      (rule != RP_SCHED_GG && rule != RP_SCHED_PAPER4 && rule != RP_SCHED_SHIFT_K))
+    return fail(RP_EINVAL, "rp_lockstep_run: bad rule, t0, steps or section_length");
+  const int world = c->cfg.world;
+  std::vector<int32_t> local, all(world);
+  std::vector<char> is_local(world, 0);
+  for (int w = 0; w < world; ++w) {
+    all[w] = w;
+    if (c->w[w].local) {
+      local.push_back(w);
+      is_local[w] = 1;
+    }
+  }
+  std::vector<rp_group> mine(local.size()), gen(world);
+  std::vector<int64_t> foreign;
+  for (int64_t s = 0; s < steps; ++s) {
+    const int64_t t = t0 + s;
+    for (int32_t w : local) {  // alg1 step 2 with the bound gradient
+      const int rc = stage_step(c, w, nullptr, lr);
+      if (rc != RP_OK) return rc;
+    }
+    foreign.clear();
+    if (t % section_length != 0) {  // no synchronization this step, SGD only
+      for (size_t i = 0; i < local.size(); ++i) {
+        mine[i] = rp_group{};
+        mine[i].seq = -(1 + t * world + local[i]);
+        mine[i].size = 1;
+        for (int j = 0; j < RP_MAX_GROUP; ++j) mine[i].members[j] = j == 0 ? local[i] : -1;
+      }
+    } else if (rule != RP_SCHED_GG) {  // static schedule S(rule, t)
+      for (size_t i = 0; i < local.size(); ++i) {
+        const int rc = rp_schedule_static_worker(c, rule, t, local[i], &mine[i]);
+        if (rc != RP_OK) return rc;
+      }
+    } else {  // GG requests of every worker in ascending order: identical on every rank
+      int rc = rp_group_generate_many(c, all.data(), world, gen.data());
+      if (rc != RP_OK) return rc;
+      std::set<int64_t> seen;
+      size_t li = 0;
+      for (int w = 0; w < world; ++w) {
+        const rp_group& g = gen[w];
+        if (is_local[w]) {
+          mine[li++] = g;
+        } else if (!seen.count(g.seq)) {
+          bool any_local = false;
+          for (int j = 0; j < g.size; ++j) any_local = any_local || is_local[g.members[j]];
+          if (!any_local) foreign.push_back(g.seq);
+        }
+        seen.insert(g.seq);
+      }
+    }
+    int rc = rp_batch_begin(c);
+    if (rc != RP_OK) return rc;
+    for (size_t i = 0; i < local.size() && rc == RP_OK; ++i) rc = rp_preduce(c, local[i], &mine[i]);
+    const int rc_end = rp_batch_end(c);
+    if (rc != RP_OK) return rc;
+    if (rc_end != RP_OK) return rc_end;
+    for (int32_t w : local) {
+      rc = rp_barrier_free_wait(c, w, RP_WAIT_DEVICE);
+      if (rc != RP_OK) return rc;
+    }
+    std::sort(foreign.begin(), foreign.end());
+    foreign.erase(std::unique(foreign.begin(), foreign.end()), foreign.end());
+    for (int64_t q : foreign) {
+      rc = rp_gg_release(c, q);
+      if (rc != RP_OK) return rc;
+    }
+  }
+  return RP_OK;
+}

@@ -32,6 +32,7 @@ RP_DTYPE_F32 = 0
 RP_DTYPE_BF16 = 1
 RP_SCHED_PAPER4 = 1
 RP_SCHED_SHIFT_K = 2
+RP_SCHED_GG = -1
 RP_WAIT_DEVICE = -1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -173,6 +174,8 @@ _SIGNATURES = {
     "rp_compute_delay": (ctypes.c_int, [_P, ctypes.c_int64]),
     "rp_fill_xi": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_uint64, _P]),
+    "rp_lockstep_run": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_float,
+                                       ctypes.c_int32]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -346,6 +349,10 @@ def rp_batch_end(ctx):
     _check(load_library().rp_batch_end(ctx), "rp_batch_end")
 
 
+def rp_lockstep_run(ctx, rule, t0, steps, lr, section_length=1):
+    _check(load_library().rp_lockstep_run(ctx, rule, t0, steps, lr, section_length), "rp_lockstep_run")
+
+
 def rp_timing_read(ctx):
     t = rp_timing()
     _check(load_library().rp_timing_read(ctx, ctypes.byref(t)), "rp_timing_read")
@@ -511,6 +518,9 @@ class Context:
 
     def batch_end(self):
         rp_batch_end(self.handle)
+
+    def lockstep_run(self, rule, t0, steps, lr=0.1, section_length=1):
+        rp_lockstep_run(self.handle, rule, t0, steps, lr, section_length)
 
     def timing_read(self):
         return rp_timing_read(self.handle)

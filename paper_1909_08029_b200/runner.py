@@ -18,7 +18,7 @@ any n_params), gradients likewise.
 import torch
 
 from . import rp
-from .rp import Context, RP_SCHED_PAPER4, RP_SCHED_SHIFT_K, RP_WAIT_DEVICE
+from .rp import Context, RP_SCHED_GG, RP_SCHED_PAPER4, RP_SCHED_SHIFT_K, RP_WAIT_DEVICE
 
 SEED_X = 1   # x_w^0[j] = xi(1, w, 0, j)
 SEED_G = 2   #                            g_w^t[j] = xi(2, w, t, j)
@@ -160,6 +160,15 @@ class LockstepRunner:
             self.ctx.gg_release(seq)
         self.t = t
         return groups
+
+    def run_native(self, steps):
+        """`steps` lockstep steps in ONE library call (rp_lockstep_run: the same sequence of
+        calls as step(), issued from C++), with the bound (resident) gradients, plain SGD."""
+        if self.grad_mode != "resident" or self.momentum is not None:
+            raise ValueError("run_native: resident gradients and plain SGD only")
+        rule = RP_SCHED_GG if self.mode == "gd" else RULES[self.rule]
+        self.ctx.lockstep_run(rule, self.t + 1, steps, self.lr, self.section_length)
+        self.t += steps
 
     def run(self, steps):
         log = []

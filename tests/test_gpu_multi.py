@@ -156,3 +156,17 @@ def test_multi_gpu_bf16_parity(gpus, spec):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, {"sample": 0, "rule": None, "dtype": "bf16", **spec})
+
+
+@pytest.mark.parametrize("gpus,spec", [
+    # rp_lockstep_run (the native step loop) across GPUs, resident gradients
+    (2, dict(wpg=4, n=100_003, k=3, mode="gd", steps=12)),
+    (2, dict(wpg=4, n=50_007, k=3, mode="gd", steps=10, ii=True)),
+    (2, dict(wpg=2, n=100_003, k=3, mode="static", rule="shift_k", steps=10)),
+    (4, dict(wpg=8, n=30_011, k=3, mode="gd", steps=8, ii=True)),
+    (4, dict(wpg=1, n=200_003, k=3, mode="gd", steps=10, dtype="bf16")),
+])
+def test_multi_gpu_native_executor(gpus, spec):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, "native": True, **spec})

@@ -196,3 +196,32 @@ def test_bf16_full_size_sampled():
         X, _ = sim.run_lockstep(8, N_R50, T, mode="gd", k=3, c_thres=4, seed_gd=3, lo=lo, hi=hi, dtype="bf16")
         _compare(r, X, lo, hi)
     r.close()
+
+
+@pytest.mark.parametrize("spec", [
+    dict(world=4, n=(1 << 20) + 3, k=2, mode="static", rule="shift_k", T=40),
+    dict(world=4, n=(1 << 16) + 1, k=2, mode="static", rule="paper4", nodes=2, T=20),
+    dict(world=8, n=(1 << 18) + 5, k=3, mode="gd", T=30),
+    dict(world=8, n=100_003, k=3, mode="gd", T=12, section_length=3),
+    dict(world=8, n=100_003, k=3, mode="gd", T=12, dtype="bf16"),
+    dict(world=8, n=60_001, k=3, mode="gd", T=10, ii_nodes=2),
+])
+def test_native_lockstep_executor(spec):
+    # rp_lockstep_run: the runner's step loop issued from C++ (resident gradients g_w = xi(2, w, 1))
+    # must reproduce the oracle bit for bit, like the per-call API
+    import paper_1909_08029_b200 as rp
+    s = dict(nodes=0, section_length=1, dtype="f32", ii_nodes=0, rule=None, **spec)
+    flags = rp.RP_FLAG_INTER_INTRA if s["ii_nodes"] else 0
+    r = LockstepRunner(s["world"], s["n"], mode=s["mode"], rule=s["rule"], group_size=s["k"], c_thres=4, seed_gd=3,
+                       nodes=s["nodes"] or s["ii_nodes"], grad_mode="resident", section_length=s["section_length"],
+                       dtype=s["dtype"], flags=flags)
+    r.run_native(s["T"] // 2)
+    r.run_native(s["T"] - s["T"] // 2)          # two calls: t0 continues where the first ended
+    r.synchronize()
+    X, _ = sim.run_lockstep(s["world"], s["n"], s["T"], mode=s["mode"], rule=s["rule"], k=s["k"], c_thres=4,
+                            seed_gd=3, nodes=s["nodes"] or None,
+                            m=(s["world"] // s["nodes"]) if s["nodes"] else None,
+                            section_length=s["section_length"], dtype=s["dtype"], grad_step=1,
+                            ii_nodes=s["ii_nodes"])
+    _compare(r, X)
+    r.close()
