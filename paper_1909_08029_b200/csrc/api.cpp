@@ -149,7 +149,8 @@ struct rp_ctx {
   int64_t trace_local_n = 0;
   cudaStream_t comm = nullptr;      // asynchronous cross-GPU launches, in GG order
   cudaStream_t aux = nullptr;       // lockstep: intra-GPU groups beside the step's cross-GPU launch
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t xs = nullptr;        // ... and the cross-GPU launch itself, at the greatest priority
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_xjoin = nullptr;
   std::set<int64_t> xready;         // cross GG groups whose local members all arrived
   std::set<int64_t> xlaunched;      // cross GG groups this GPU has launched
   rp_stats stats{};
@@ -324,19 +325,29 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     if (ok) fused.swap(seqs);
   }
   cudaStream_t intra_stream = L.stream;
+  static int tpc = -1;  // RP_DYN_TPC: tiles per CTA of the intra-GPU launch in split mode
+  if (tpc < 0) {
+    const char* v = std::getenv("RP_DYN_TPC");
+    tpc = v && *v ? std::atoi(v) : 128;
+  }
   if (split) {
     CUDA_TRY(cudaEventRecord(c->ev_fork, L.stream));
     CUDA_TRY(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->xs, c->ev_fork, 0));
     intra_stream = c->aux;
-    const int rc = launch_cross(c, cross, {}, L.stream, split_ctas);
+    const int rc = launch_cross(c, cross, {}, c->xs, split_ctas);
     if (rc != RP_OK) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_xjoin, c->xs));
   }
   // One fused launch for all remaining intra-GPU groups (chunked at kMaxTasks
   // groups / kMaxTaskMembers members).
   size_t gi = 0;
   while (gi < seqs.size()) {
     rp::MultiTask t{};
-    if (split) t.reserve_sms = split_ctas;  // xgpu: at most one CTA per SM at first
+    if (split) {
+      t.reserve_sms = split_ctas;  // beside a cross launch: dynamic-tile kernel, one stage less
+      t.tiles_per_cta = tpc;       // retiring CTAs: the cross launch's CTAs find free slots
+    }
     int nm = 0;
     int64_t bytes = 0;
     while (gi < seqs.size() && t.ngroups < rp::kMaxTasks) {
@@ -380,6 +391,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (split) {
     CUDA_TRY(cudaEventRecord(c->ev_join, c->aux));
     CUDA_TRY(cudaStreamWaitEvent(L.stream, c->ev_join, 0));
+    CUDA_TRY(cudaStreamWaitEvent(L.stream, c->ev_xjoin, 0));
   } else if (!nv.empty()) {
     const int rc = launch_nvls_groups(c, nv, L.stream);
     if (rc != RP_OK) return rc;
@@ -765,6 +777,17 @@ cudaError_t create_aux_stream(cudaStream_t* s) {
 }
 }  // namespace
 
+// Stream of the cross-GPU launch in split mode: the greatest priority, so its CTAs take SM
+// slots ahead of the retiring CTAs of the intra-GPU launch beside it (RP_XS_PRIO=0: default).
+static cudaError_t create_cross_stream(cudaStream_t* s) {
+  const char* v = std::getenv("RP_XS_PRIO");
+  if (v && *v && std::atoi(v) == 0) return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, greatest);
+}
+
 int rp_init(const rp_config* cfg, rp_ctx** out) {
   if (!cfg || !out) return fail(RP_EINVAL, "rp_init: null argument");
   *out = nullptr;
@@ -834,8 +857,10 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
     if (k.n_gpus > 1) {
       if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess ||
           (e = create_aux_stream(&c->aux)) != cudaSuccess ||
+          (e = create_cross_stream(&c->xs)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess) {
+          (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&c->ev_xjoin, cudaEventDisableTiming)) != cudaSuccess) {
         rp_finalize(c);
         return cuda_fail(e, "rp_init: comm streams");
       }
@@ -989,8 +1014,13 @@ int rp_finalize(rp_ctx* c) {
       cudaStreamSynchronize(c->aux);
       cudaStreamDestroy(c->aux);
     }
+    if (c->xs) {
+      cudaStreamSynchronize(c->xs);
+      cudaStreamDestroy(c->xs);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_xjoin) cudaEventDestroy(c->ev_xjoin);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     cudaDeviceSynchronize();
     rp::nvls_teardown(&c->nvls);

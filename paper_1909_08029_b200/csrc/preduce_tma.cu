@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -535,17 +536,21 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
   __syncthreads();
   if (warp == kWsConsumers) {  // producer
     if (lane == 0) {
+      // t.tiles_per_cta > 0: the CTA retires after that many tiles, so the block scheduler
+      // regularly frees SM slots (a concurrent cross-GPU launch on a higher-priority stream
+      // takes them first); 0: persistent until the counter runs out
+      const int64_t quota = t.tiles_per_cta > 0 ? t.tiles_per_cta : INT64_MAX;
       int64_t next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
       for (int64_t it = 0;; ++it) {
         const int s = static_cast<int>(it % S);
         if (it >= S) mbar_wait(&empty[s], static_cast<uint32_t>((it / S - 1) & 1));
-        const int64_t id = next;
+        const int64_t id = it < quota ? next : total;
         tile_of[s] = id;
         if (id >= total) {
           mbar_arrive(&full[s]);  // end marker: phase completes with no bytes
           break;
         }
-        next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
+        if (it + 1 < quota) next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
         const int g = static_cast<int>(id % t.ngroups);
         const int first = t.group_first[g], K = t.group_k[g];
         const int64_t base = (id / t.ngroups) * T;
@@ -703,8 +708,14 @@ int launch_dyn(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
   if (!ring) return RP_ECUDA;
   static std::atomic<uint64_t> next_slot{0};
   int* ctr = reinterpret_cast<int*>(ring + 2 * (next_slot.fetch_add(1) % kDynSlots));
-  const int grid = sms() * C;
-  preduce_dyn_kernel<KMAX, T, S, C, BF><<<grid, kWsThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n, ctr);
+  int64_t grid = static_cast<int64_t>(sms()) * C;
+  if (t.tiles_per_cta > 0) {  // enough retiring CTAs to cover every tile
+    const int64_t per = BF ? 8 : 4;
+    const int64_t tiles = ((n / per) + T - 1) / T * t.ngroups;
+    grid = std::max<int64_t>(1, (tiles + t.tiles_per_cta - 1) / t.tiles_per_cta);
+  }
+  preduce_dyn_kernel<KMAX, T, S, C, BF><<<static_cast<unsigned>(grid), kWsThreads, smem, stream>>>(t, n / (BF ? 8 : 4), n,
+                                                                                                ctr);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("preduce_dyn launch: ") + cudaGetErrorString(e);

@@ -210,7 +210,7 @@ def test_native_lockstep_executor(spec):
     # rp_lockstep_run: the runner's step loop issued from C++ (resident gradients g_w = xi(2, w, 1))
     # must reproduce the oracle bit for bit, like the per-call API
     import paper_1909_08029_b200 as rp
-    s = dict(nodes=0, section_length=1, dtype="f32", ii_nodes=0, rule=None, **spec)
+    s = {**dict(nodes=0, section_length=1, dtype="f32", ii_nodes=0, rule=None), **spec}
     flags = rp.RP_FLAG_INTER_INTRA if s["ii_nodes"] else 0
     r = LockstepRunner(s["world"], s["n"], mode=s["mode"], rule=s["rule"], group_size=s["k"], c_thres=4, seed_gd=3,
                        nodes=s["nodes"] or s["ii_nodes"], grad_mode="resident", section_length=s["section_length"],
