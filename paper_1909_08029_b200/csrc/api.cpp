@@ -328,7 +328,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   static int tpc = -1;  // RP_DYN_TPC: tiles per CTA of the intra-GPU launch in split mode
   if (tpc < 0) {
     const char* v = std::getenv("RP_DYN_TPC");
-    tpc = v && *v ? std::atoi(v) : 128;
+    tpc = v && *v ? std::atoi(v) : 0;
   }
   if (split) {
     CUDA_TRY(cudaEventRecord(c->ev_fork, L.stream));
@@ -777,11 +777,12 @@ cudaError_t create_aux_stream(cudaStream_t* s) {
 }
 }  // namespace
 
-// Stream of the cross-GPU launch in split mode: the greatest priority, so its CTAs take SM
-// slots ahead of the retiring CTAs of the intra-GPU launch beside it (RP_XS_PRIO=0: default).
+// Stream of the cross-GPU launch in split mode. RP_XS_PRIO=1 gives it the greatest priority,
+// so its CTAs take SM slots ahead of retiring CTAs of the intra-GPU launch (with RP_DYN_TPC):
+// steadier at N = 2, slower at N = 4 (profiles/r01_split/, profiles/r01_final3_4gpu/): off.
 static cudaError_t create_cross_stream(cudaStream_t* s) {
   const char* v = std::getenv("RP_XS_PRIO");
-  if (v && *v && std::atoi(v) == 0) return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  if (!(v && *v && std::atoi(v) == 1)) return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
   int least = 0, greatest = 0;
   cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
   if (e != cudaSuccess) return e;

@@ -462,6 +462,7 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_ws_kernel(const MultiTa
 // stage's mbarrier arrive, release/acquire at CTA scope). The last CTA to finish resets the
 // launch's counter pair, so the next launch that takes this ring slot finds zeros.
 constexpr int kDynSlots = 4096;
+constexpr int kDynBatch = 4;  // tile ids per atomic
 
 template <int K, int T, bool BF>
 __device__ __forceinline__ void dyn_consume(const MultiTask& t, int g, int64_t base, int cnt, const float4* stage,
@@ -539,18 +540,27 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
       // t.tiles_per_cta > 0: the CTA retires after that many tiles, so the block scheduler
       // regularly frees SM slots (a concurrent cross-GPU launch on a higher-priority stream
       // takes them first); 0: persistent until the counter runs out
-      const int64_t quota = t.tiles_per_cta > 0 ? t.tiles_per_cta : INT64_MAX;
-      int64_t next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
+      // Tile ids are drawn kDynBatch at a time (one atomic per batch: a single-group launch
+      // needs ~4e8 tiles/s, more than one L2 address serves), the next batch one batch ahead.
+      unsigned long long* const c0 = reinterpret_cast<unsigned long long*>(ctr);
+      const int64_t quota = t.tiles_per_cta > 0
+                                ? (static_cast<int64_t>(t.tiles_per_cta) + kDynBatch - 1) / kDynBatch * kDynBatch
+                                : INT64_MAX;
+      int64_t batch = static_cast<int64_t>(atomicAdd(c0, static_cast<unsigned long long>(kDynBatch)));
+      int64_t nextb = 0;
       for (int64_t it = 0;; ++it) {
         const int s = static_cast<int>(it % S);
         if (it >= S) mbar_wait(&empty[s], static_cast<uint32_t>((it / S - 1) & 1));
-        const int64_t id = it < quota ? next : total;
+        const int j = static_cast<int>(it % kDynBatch);
+        if (j == 0 && it > 0) batch = nextb;
+        if (j == 0 && it + kDynBatch < quota)
+          nextb = static_cast<int64_t>(atomicAdd(c0, static_cast<unsigned long long>(kDynBatch)));
+        const int64_t id = it < quota ? batch + j : total;
         tile_of[s] = id;
         if (id >= total) {
           mbar_arrive(&full[s]);  // end marker: phase completes with no bytes
           break;
         }
-        if (it + 1 < quota) next = atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
         const int g = static_cast<int>(id % t.ngroups);
         const int first = t.group_first[g], K = t.group_k[g];
         const int64_t base = (id / t.ngroups) * T;
