@@ -462,7 +462,6 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_ws_kernel(const MultiTa
 // stage's mbarrier arrive, release/acquire at CTA scope). The last CTA to finish resets the
 // launch's counter pair, so the next launch that takes this ring slot finds zeros.
 constexpr int kDynSlots = 4096;
-constexpr int kDynBatch = 4;  // tile ids per atomic
 
 template <int K, int T, bool BF>
 __device__ __forceinline__ void dyn_consume(const MultiTask& t, int g, int64_t base, int cnt, const float4* stage,
@@ -543,6 +542,7 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
       // Tile ids are drawn kDynBatch at a time (one atomic per batch: a single-group launch
       // needs ~4e8 tiles/s, more than one L2 address serves), the next batch one batch ahead.
       unsigned long long* const c0 = reinterpret_cast<unsigned long long*>(ctr);
+      const int kDynBatch = t.dyn_batch > 0 ? t.dyn_batch : 1;
       const int64_t quota = t.tiles_per_cta > 0
                                 ? (static_cast<int64_t>(t.tiles_per_cta) + kDynBatch - 1) / kDynBatch * kDynBatch
                                 : INT64_MAX;
@@ -714,6 +714,10 @@ int launch_dyn(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     }
     attr = true;
   }
+  // tile ids per atomic: 1 keeps the window tightest when 3+ groups share the launch (cfg 2:
+  // 0.3615 vs 0.367 ms); 4 for 1-2 groups, where one id per atomic leaves the producer
+  // waiting on a single contended L2 address (profiles/r01_kernel_choice/)
+  t.dyn_batch = t.ngroups >= 3 ? 1 : 4;
   unsigned long long* ring = dyn_counters(err);
   if (!ring) return RP_ECUDA;
   static std::atomic<uint64_t> next_slot{0};
@@ -814,6 +818,17 @@ int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string*
   for (int i = 0; i < nm; ++i)
     if (t.u[i].v != nullptr) return RP_EINVAL;  // momentum: LDG kernel
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // variant 7 (dynamic tiles) pays off on large launches; below ~1 GB of algorithmic traffic
+  // (e.g. one lone SGD worker of ResNet-50 size: 0.0763 vs 0.0518 ms) the statically split
+  // kernel is faster, unless a concurrent cross-GPU launch needs the dynamic one
+  static int64_t min_bytes = -1;  // RP_DYN_MIN_BYTES (tests set 0 to force variant 7 everywhere)
+  if (min_bytes < 0) {
+    const char* v = std::getenv("RP_DYN_MIN_BYTES");
+    min_bytes = v && *v ? std::atoll(v) : (int64_t{1} << 30);
+  }
+  const int64_t launch_bytes = static_cast<int64_t>(nm) * n * (bf16 ? 6 : 12);
+  if (variant == 7 && t.reserve_sms == 0 && launch_bytes < min_bytes && kmax <= 8)
+    return bf16 ? launch_ws_variant<true>(6, kmax, t, n, s, err) : launch_ws_variant<false>(5, kmax, t, n, s, err);
   if ((variant == 7 || t.reserve_sms > 0) && kmax <= 8)
     return bf16 ? launch_dyn_variant<true>(kmax, t, n, s, err) : launch_dyn_variant<false>(kmax, t, n, s, err);
   if ((variant == 5 || variant == 6) && kmax <= 8) {

@@ -95,6 +95,7 @@ struct MultiTask {
   int32_t cta_begin[kMaxTasks + 1];
   int32_t reserve_sms;  // SMs left to a concurrent cross-GPU launch (0 = use every SM)
   int32_t tiles_per_cta;  // dynamic-tile kernel: CTAs retire after this many tiles (0 = persistent)
+  int32_t dyn_batch;      // dynamic-tile kernel: tile ids per atomic (set by the launcher)
 };
 
 // Fused SGD + P-Reduce of groups whose members all live on the current GPU.
