@@ -548,22 +548,29 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
                                 : INT64_MAX;
       int64_t batch = static_cast<int64_t>(atomicAdd(c0, static_cast<unsigned long long>(kDynBatch)));
       int64_t nextb = 0;
-      for (int64_t it = 0;; ++it) {
-        const int s = static_cast<int>(it % S);
-        if (it >= S) mbar_wait(&empty[s], static_cast<uint32_t>((it / S - 1) & 1));
-        const int j = static_cast<int>(it % kDynBatch);
-        if (j == 0 && it > 0) batch = nextb;
+      int j = 0, s = 0;
+      uint32_t phase = 0;
+      for (int64_t it = 0;; ++it) {  // no divisions on the producer's critical path
+        if (it >= S) mbar_wait(&empty[s], phase ^ 1u);
+        if (j == kDynBatch) {
+          batch = nextb;
+          j = 0;
+        }
         if (j == 0 && it + kDynBatch < quota)
           nextb = static_cast<int64_t>(atomicAdd(c0, static_cast<unsigned long long>(kDynBatch)));
         const int64_t id = it < quota ? batch + j : total;
+        ++j;
         tile_of[s] = id;
         if (id >= total) {
           mbar_arrive(&full[s]);  // end marker: phase completes with no bytes
           break;
         }
-        const int g = static_cast<int>(id % t.ngroups);
+        const uint32_t id32 = static_cast<uint32_t>(id);  // total < 2^31 (checked by the launcher)
+        const uint32_t ng = static_cast<uint32_t>(t.ngroups);
+        const uint32_t tq = id32 / ng;
+        const int g = static_cast<int>(id32 - tq * ng);
         const int first = t.group_first[g], K = t.group_k[g];
-        const int64_t base = (id / t.ngroups) * T;
+        const int64_t base = static_cast<int64_t>(tq) * T;
         const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(T), n4 - base) * 16);
         uint32_t tot = 0;
         for (int m = 0; m < K; ++m) tot += t.u[first + m].g ? 2 * bytes : bytes;
@@ -572,6 +579,10 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
           bulk_load(stage + (s * 2 * KMAX + 2 * m) * T, t.x[first + m] + 4 * base, bytes, &full[s]);
           if (t.u[first + m].g)
             bulk_load(stage + (s * 2 * KMAX + 2 * m + 1) * T, t.u[first + m].g + 4 * base, bytes, &full[s]);
+        }
+        if (++s == S) {
+          s = 0;
+          phase ^= 1u;
         }
       }
     }
@@ -586,8 +597,10 @@ __global__ void __launch_bounds__(kWsThreads, C) preduce_dyn_kernel(const MultiT
       mbar_wait(&full[s], static_cast<uint32_t>((it / S) & 1));
       const int64_t id = tile_of[s];
       if (id >= total) break;
-      const int g = static_cast<int>(id % t.ngroups);
-      const int64_t base = (id / t.ngroups) * T;
+      const uint32_t ng = static_cast<uint32_t>(t.ngroups);
+      const uint32_t tq = static_cast<uint32_t>(id) / ng;
+      const int g = static_cast<int>(static_cast<uint32_t>(id) - tq * ng);
+      const int64_t base = static_cast<int64_t>(tq) * T;
       const int cnt = static_cast<int>(min(static_cast<int64_t>(T), n4 - base));
       const int s2 = s * 2 * KMAX;
       const int K = t.group_k[g];
@@ -714,10 +727,19 @@ int launch_dyn(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
     }
     attr = true;
   }
-  // tile ids per atomic: 1 keeps the window tightest when 3+ groups share the launch (cfg 2:
-  // 0.3615 vs 0.367 ms); 4 for 1-2 groups, where one id per atomic leaves the producer
-  // waiting on a single contended L2 address (profiles/r01_kernel_choice/)
-  t.dyn_batch = t.ngroups >= 3 ? 1 : 4;
+  // tile ids per atomic (sweep profiles/r01_kernel_choice/batch_sweep.txt, ms/step at N=1):
+  // 1: cfg2 0.3616, cfg2ii 0.3785, bf16 0.1934; 2: 0.3639, 0.3640, 0.1905; 4: 0.3669, 0.3661,
+  // 0.1926; 8: 0.3715, 0.3708, 0.1966 -> 2 for every launch (RP_DYN_BATCH overrides)
+  static int batch_env = -1;  // RP_DYN_BATCH: tile ids per atomic (0 = default 2)
+  if (batch_env < 0) {
+    const char* v = std::getenv("RP_DYN_BATCH");
+    batch_env = v && *v ? std::atoi(v) : 0;
+  }
+  t.dyn_batch = batch_env > 0 ? batch_env : 2;
+  if ((n / (BF ? 8 : 4) + T) / T * t.ngroups >= (int64_t{1} << 31)) {
+    *err = "preduce_dyn: more than 2^31 tiles";
+    return RP_EINVAL;
+  }
   unsigned long long* ring = dyn_counters(err);
   if (!ring) return RP_ECUDA;
   static std::atomic<uint64_t> next_slot{0};
