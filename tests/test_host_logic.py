@@ -59,7 +59,8 @@ def test_schedule_rule_errors():
 
 
 @pytest.mark.parametrize("n,k,c_thres,seed", [(8, 3, 4, 3), (16, 3, 4, 7), (16, 2, 0, 1), (5, 4, 2, 99),
-                                              (64, 16, 0, 5), (12, 5, 3, 2**63 + 11)])
+                                              (64, 16, 0, 5), (12, 5, 3, 2**63 + 11),
+                                              (64, 3, 4, 3)])   # bench cfg2 at N = 8
 def test_gg_lockstep_bit_exact(n, k, c_thres, seed):
     og = GroupGenerator(n, k, c_thres=c_thres, seed_gd=seed)
     with rp.Context(n, 1024, n_gpus=0, group_size=k, c_thres=c_thres, seed_gd=seed) as c:
@@ -175,7 +176,8 @@ def test_random_gg_interleavings_bit_exact(n, k, seed, tmp_path):
     sim.replay_trace(events, n, 16, k=k, c_thres=0, seed_gd=seed, policy="random")
 
 
-@pytest.mark.parametrize("nodes,m,k,c_thres", [(4, 4, 3, 0), (2, 8, 3, 4), (8, 2, 2, 0), (1, 8, 3, 0), (3, 5, 4, 2)])
+@pytest.mark.parametrize("nodes,m,k,c_thres", [(4, 4, 3, 0), (2, 8, 3, 4), (8, 2, 2, 0), (1, 8, 3, 0), (3, 5, 4, 2),
+                                            (8, 8, 3, 0)])   # bench cfg2ii at N = 8
 def test_inter_intra_lockstep_bit_exact(nodes, m, k, c_thres):
     n = nodes * m
     og = GroupGenerator(n, k, c_thres=c_thres, seed_gd=9, nodes=nodes)
