@@ -77,8 +77,22 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Watchdog: a peer that never posts its flag (a crashed rank, a broken collective contract)
+// traps the kernel after kWaitTrapNs instead of spinning forever, so the process fails with a
+// CUDA error rather than hanging the GPU. The clock is read once per 4096 polls.
+constexpr unsigned long long kWaitTrapNs = 30ull * 1000 * 1000 * 1000;
 __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long tag) {
-  while (ld_acquire_sys(f) != tag) __nanosleep(32);
+  if (ld_acquire_sys(f) == tag) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (unsigned n = 1; ld_acquire_sys(f) != tag; ++n) {
+    __nanosleep(32);
+    if ((n & 4095u) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > kWaitTrapNs) __trap();
+    }
+  }
 }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));

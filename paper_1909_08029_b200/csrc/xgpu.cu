@@ -97,8 +97,22 @@ __device__ __forceinline__ unsigned long long* flag_at(unsigned long long* base,
          (kind == kFlagA ? c : (kind == kFlagB ? kMaxChunks + c : 2 * kMaxChunks));
 }
 
+// Watchdog: a peer that never posts its flag (a crashed rank, a broken collective contract)
+// traps the kernel after kWaitTrapNs instead of spinning forever, so the process fails with a
+// CUDA error rather than hanging the GPU. The clock is read once per 4096 polls.
+constexpr unsigned long long kWaitTrapNs = 30ull * 1000 * 1000 * 1000;
 __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long tag) {
-  while (ld_acquire_sys(f) != tag) __nanosleep(32);
+  if (ld_acquire_sys(f) == tag) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (unsigned n = 1; ld_acquire_sys(f) != tag; ++n) {
+    __nanosleep(32);
+    if ((n & 4095u) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > kWaitTrapNs) __trap();
+    }
+  }
 }
 
 // ---- element access: fp32 replicas, or bf16 replicas with fp32 arithmetic (reading R26) ----
