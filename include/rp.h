@@ -80,6 +80,12 @@ extern "C" {
                                    Division queues an Inter group (Head Workers across
                                    nodes, the rest node-local) and an Intra group (whole
                                    node); nodes = cfg.nodes, or n_gpus when 0           */
+#define RP_FLAG_EMULATE 0x20    /* parity tool: n_gpus VIRTUAL GPUs on one device, one
+                                   process (rank 0, every worker local): cross-GPU
+                                   groups run the cross-GPU kernel for every virtual GPU
+                                   in ONE cooperative launch (flags, staging, partial
+                                   fold and pushes as across real GPUs); lockstep batches
+                                   only, no NVLS, no peer export/import                 */
 
 /* Replica / gradient storage (reading R26). Arithmetic is fp32
  * in the pinned order of reading R1 for both; bf16 widens exactly on load and rounds the mean
@@ -107,7 +113,10 @@ typedef struct rp_config {
   int32_t flags;           /* RP_FLAG_*                                                  */
   int32_t dtype;           /* RP_DTYPE_*: storage type of replicas and gradients (0 = fp32) */
   uint64_t job_id;         /* RP_FLAG_SHARED_GG: same nonzero value on every rank        */
-  int32_t reserved[4];
+  int32_t watchdog_s;      /* cross-GPU flag-wait limit in seconds: 0 = default (600),
+                              < 0 = wait forever; env RP_WATCHDOG_S overrides. A wait past
+                              it is recorded and reported as RP_ETIMEOUT (rp_check)        */
+  int32_t reserved[3];
 } rp_config;
 
 /* One group: members ascending. seq >= 0: granted by the GG (creation order);
@@ -151,6 +160,16 @@ typedef struct rp_timing {
   int64_t cross_bytes_nvlink;
   int64_t cross_bytes_hbm;    /* local HBM bytes of the cross launches (incl. fused groups) */
 } rp_timing;
+
+/* One timed launch (RP_FLAG_TIMING), in launch order: rp_timing_records. */
+typedef struct rp_launch_record {
+  double ms;                  /* CUDA-event duration on the launching stream            */
+  int64_t bytes_hbm;          /* algorithmic HBM bytes of the launch                    */
+  int64_t bytes_nvlink;       /* algorithmic NVLink bytes this GPU stores into peers    */
+  int64_t batch;              /* rp_batch_end calls before it (= lockstep step index)   */
+  int32_t cross;              /* 1 = cross-GPU (or NVLS) kernel, 0 = intra-GPU kernel    */
+  int32_t reserved;
+} rp_launch_record;
 
 typedef struct rp_ctx rp_ctx;
 
@@ -355,6 +374,12 @@ int rp_stats_get(rp_ctx* ctx, rp_stats* out);
  * reset the accumulator. Errors: RP_ESTATE (context created without
  * RP_FLAG_TIMING), RP_ECUDA. */
 int rp_timing_read(rp_ctx* ctx, rp_timing* out);
+
+/* Did a cross-GPU (or NVLS) flag wait of a COMPLETED launch pass the watchdog limit
+ * (rp_config.watchdog_s)? RP_OK, or RP_ETIMEOUT with rp_last_error() naming the GPU, the
+ * peer, the flag kind, the chunk and the tags. After a timeout the replicas of the groups
+ * of that step are undefined. rp_barrier_free_wait and rp_lockstep_run check it too. */
+int rp_check(rp_ctx* ctx);
 /* Start writing the JSONL decision trace (req / done / retire in GG order)
  * to `path` (truncates). The oracle replays it (tests/). */
 int rp_trace_open(rp_ctx* ctx, const char* path);
@@ -370,12 +395,35 @@ int rp_abi_version(void);
  * P:1395; reading R13). Errors: RP_EINVAL (ns < 0), RP_ECUDA. */
 int rp_compute_delay(void* stream, int64_t ns);
 
+/* Synthetic compute of worker w for the heterogeneity runs (reading R13): rp_lockstep_run
+ * enqueues rp_compute_delay(ns) on w's stream at the start of each of w's steps, before its
+ * rp_step (0 = none). Ordering stays group-local: a slow worker delays only the groups it
+ * joins, through its arrival event. Errors: RP_EINVAL (w not local, ns < 0), RP_ENODEV. */
+int rp_set_compute_delay(rp_ctx* ctx, int32_t w, int64_t ns);
+
 /* dst[i] = xi(seed, w, t, j0 + i) for i < n on `stream` (cudaStream_t as void*),
  * the counter-based generator of DESIGN.md "Input recipe" (splitmix64
  * finalizer; bit-identical to rp_inputs/gen.py). dst must be 4-byte aligned
  * device memory. Errors: RP_EINVAL, RP_ECUDA. */
 int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                void* stream);
+
+/* ---- NCCL-baseline helpers (bench.py --impl nccl / nccl-group; NOT the method's path) ----
+ * The paper's P-Reduce is an NCCL all-reduce on a per-group communicator;
+ * with several simulated workers per GPU a baseline needs a local pre-sum and a local
+ * broadcast of the mean (one NCCL rank per GPU). Buffers: device memory of the current GPU,
+ * 16-byte aligned, n fp32 elements; 1 <= m <= 16 members. Errors: RP_EINVAL, RP_ECUDA.
+ *   rp_bench_presum:       out = left fold over m of fl(x_i - fl(lr g_i))   (x, g read once)
+ *   rp_bench_scatter_mean: x_i = fl(s / k) for every member i                (s read once) */
+int rp_bench_presum(const float* const* x, const float* const* g, int32_t m, int64_t n, float lr, float* out,
+                    void* stream);
+int rp_bench_scatter_mean(const float* s, int64_t n, float k, float* const* x, int32_t m, void* stream);
+
+/* Per-launch timing records (RP_FLAG_TIMING): copies up to `cap` completed launches (oldest
+ * first) into out, sets *n, and drops them (like rp_timing_read, which aggregates instead).
+ * Blocks until those launches completed. Errors: RP_EINVAL, RP_ESTATE (no RP_FLAG_TIMING),
+ * RP_ECUDA. */
+int rp_timing_records(rp_ctx* ctx, rp_launch_record* out, int32_t cap, int32_t* n);
 
 /* Native lockstep executor (alg1, for every local worker of this rank): runs
  * `steps` iterations t = t0, t0 + 1, ... (t0 >= 1) exactly as the per-call sequence

@@ -53,11 +53,15 @@ def momentum_sgd_fp32(x, g, v, lr, mu, wd):
 
 def bf16_round(x):
     """fp32 -> bfloat16, IEEE round-to-nearest-even on the 16 dropped mantissa bits; returned
-    as float32 holding the bf16 value (finite inputs; overflow rounds to inf as IEEE does).
+    as float32 holding the bf16 value (overflow rounds to inf as IEEE does; a NaN stays a NaN).
     bf16 = the upper 16 bits of a binary32: add 0x7FFF plus the lowest kept bit, truncate."""
     b = np.ascontiguousarray(x, dtype=F32).view(np.uint32).astype(np.uint64)
     keep_lsb = (b >> np.uint64(16)) & np.uint64(1)
     r = ((b + np.uint64(0x7FFF) + keep_lsb) >> np.uint64(16)) << np.uint64(16)
+    # NaN stays NaN (reading R26): the carry above could turn a NaN into +-0 or +-inf; keep
+    # its top 16 bits and set the quiet bit instead (IEEE 754 conversion of a NaN is a NaN)
+    nan = (b & np.uint64(0x7FFFFFFF)) > np.uint64(0x7F800000)
+    r = np.where(nan, ((b >> np.uint64(16)) | np.uint64(0x40)) << np.uint64(16), r)
     return r.astype(np.uint32).view(F32)
 
 

@@ -66,6 +66,7 @@ struct WorkerSlot {
   rp::MemberUpdate upd{};  // the staged alg1 step 2
   bool in_group = false;  // arrived at a group and not yet waited
   int64_t seq = 0;
+  int64_t delay_ns = 0;   // rp_set_compute_delay: synthetic compute per rp_lockstep_run step
 };
 
 struct ActiveGroup {
@@ -161,7 +162,9 @@ struct rp_ctx {
     cudaEvent_t start, stop;
     int64_t bytes_hbm, bytes_nvlink;
     bool cross;
+    int64_t batch;
   };
+  int64_t batches = 0;                // rp_batch_end calls (lockstep step index)
   std::vector<Timed> timed;           // recorded, not yet read
   std::vector<cudaEvent_t> event_pool;  // timing events for reuse
   // multi-GPU
@@ -179,6 +182,18 @@ struct rp_ctx {
   std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
   int32_t peer_pid[RP_MAX_GPUS] = {};               // process ids (NVLS descriptor sockets)
   rp::NvlsState nvls;                               // multicast objects (rp_nvls_enable)
+  // cross-GPU flag tags: launches of groups with a given slot that involved both GPUs, counted
+  // on each side in launch order (lockstep: step order; asynchronous: ticket order), so a tag is
+  // unique per (group launch, GPU pair) and stale flags of earlier launches never match
+  uint64_t pair_tag[RP_MAX_GPUS][rp::kFlagSlots][RP_MAX_GPUS] = {};
+  rp::XErr* xerr = nullptr;                         // host-mapped watchdog record
+  rp::XErr* xerr_dev = nullptr;                     // its device address
+  unsigned long long watchdog_ns = 0;               // flag-wait limit (0 = off)
+  // RP_FLAG_EMULATE: n_gpus virtual GPUs on one device (every worker local to this process)
+  bool emulate = false;
+  unsigned long long* vflags = nullptr;             // n_gpus flag arrays
+  float* vstage = nullptr;                          // n_gpus * wpg staging regions
+  rp::XTask* d_tasks = nullptr;                     // device copy of the emulated launch's tasks
 };
 
 namespace {
@@ -260,8 +275,7 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // local (caller holds mu). The kernel runs on the stream of the lowest local
 // member after every member's arrival event; every member's stream is then
 // ordered after the kernel and records its own completion event.
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
-                 cudaStream_t stream, int max_ctas = 0);
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream, int max_ctas = 0);
 int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream);
 int pump_cross(rp_ctx* c);
 
@@ -276,12 +290,33 @@ bool nvls_group(const rp_ctx* c, const rp_group& g) {
 }
 int open_shared_gg(rp_ctx* c);
 
+// Does the group span GPUs (real or, with RP_FLAG_EMULATE, virtual)?
+bool is_cross(const rp_ctx* c, const ActiveGroup& a) {
+  return c->emulate ? __builtin_popcount(gpu_mask(c, a.g)) > 1 : a.local_mask != a.members_mask;
+}
+
+// The host-mapped watchdog record: a cross-GPU (or NVLS) flag wait that gave up.
+int check_xerr(rp_ctx* c) {
+  if (!c->xerr) return RP_OK;
+  if (!__atomic_load_n(&c->xerr->code, __ATOMIC_ACQUIRE)) return RP_OK;
+  rp::XErr e;
+  std::memcpy(&e, c->xerr, sizeof(e));
+  static const char* kinds[] = {"A (partial)", "B (mean)", "READY"};
+  const std::string kind = e.kind >= 0 && e.kind < 3 ? kinds[e.kind] : (e.kind >= 16 ? "NVLS" : "?");
+  return fail(RP_ETIMEOUT, "cross-GPU flag wait timed out after " + std::to_string(c->watchdog_ns / 1000000000ull) +
+                               " s on GPU " + std::to_string(e.gpu) + ": flag " + kind + " of chunk " +
+                               std::to_string(e.chunk) + " from GPU " + std::to_string(e.src) + " (slot " +
+                               std::to_string(e.slot) + ") expected tag " + std::to_string(e.tag) + ", holds " +
+                               std::to_string(e.seen) + " (a peer never arrived or the collective contract broke; "
+                               "the replicas of this step are undefined)");
+}
+
 int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (all_seqs.empty()) return RP_OK;
   std::vector<int64_t> seqs, cross, nv;  // intra-GPU, push cross-GPU, NVLS cross-GPU
   for (int64_t q : all_seqs) {
     const ActiveGroup& a = c->active.at(q);
-    (a.local_mask == a.members_mask ? seqs : (nvls_group(c, a.g) ? nv : cross)).push_back(q);
+    (!is_cross(c, a) ? seqs : (nvls_group(c, a.g) ? nv : cross)).push_back(q);
   }
   uint64_t all = 0;
   for (int64_t q : all_seqs) {
@@ -296,34 +331,17 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   WorkerSlot& L = c->w[launcher];
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if (((all >> m) & 1) && m != launcher) CUDA_TRY(cudaStreamWaitEvent(L.stream, c->w[m].ev_arrive, 0));
-  // With cross-GPU groups in the batch the intra-GPU groups run BESIDE them: the cross
-  // launch (NVLink-bound; grid capped at RP_XGPU_SPLIT CTAs, default 296 = every resident
-  // slot) is issued first, the intra-GPU launch (HBM-bound, dynamic-tile TMA kernel) runs on
-  // a second stream and its CTAs take SMs as they free up, drawing tiles at run time
-  // (RP_XGPU_SPLIT=0: the older mode, intra-GPU groups of <= 4 members fused into the cross
-  // launch as L items; sweep profiles/r01_split/).
+  // With cross-GPU groups in the batch the intra-GPU groups run BESIDE them: the cross launch
+  // (NVLink-bound; grid capped at RP_XGPU_SPLIT CTAs, default 296 = every resident slot) is issued
+  // first on its own stream, the intra-GPU launch (HBM-bound, dynamic-tile TMA kernel, one stage
+  // less) on a second stream; its CTAs take SM slots next to the cross kernel's and as they free
+  // up, drawing tiles at run time. Emulated GPUs (RP_FLAG_EMULATE) run the two one after the other.
   static int split_ctas = -1;
   if (split_ctas < 0) {
     const char* v = std::getenv("RP_XGPU_SPLIT");
     split_ctas = v && *v ? std::atoi(v) : 296;
   }
-  // Only when the cross-GPU work is ONE part (e.g. the Head Workers' group of Inter-Intra,
-  // §5.2): with several parts the cross kernel needs every SM (measured, profiles/r01_split/).
-  // The decision is per GPU; the cross kernel's chunk geometry does not depend on it.
-  // ... and only when the intra-GPU work clearly dominates the step (at least twice the cross
-  // part's local members): a lone intra-GPU singleton beside a cross part (cfg 4) is faster fused
-  const bool bf16 = c->cfg.dtype == RP_DTYPE_BF16;
-  int intra_members = 0, cross_members = 0;
-  for (int64_t q : seqs) intra_members += c->active.at(q).g.size;
-  for (int64_t q : cross) cross_members += __builtin_popcountll(c->active.at(q).local_mask);
-  const bool split = cross.size() == 1 && nv.empty() && !seqs.empty() && split_ctas > 0 && c->aux &&
-                     intra_members >= 2 * cross_members;
-  std::vector<int64_t> fused;
-  if (!cross.empty() && !split && !bf16) {  // bf16: intra-GPU groups keep their own launch
-    bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
-    for (int64_t q : seqs) ok = ok && c->active.at(q).g.size <= rp::kMaxFusedK;
-    if (ok) fused.swap(seqs);
-  }
+  const bool split = !cross.empty() && nv.empty() && !seqs.empty() && !c->emulate && c->aux && c->xs;
   cudaStream_t intra_stream = L.stream;
   static int tpc = -1;  // RP_DYN_TPC: tiles per CTA of the intra-GPU launch in split mode
   if (tpc < 0) {
@@ -335,7 +353,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     CUDA_TRY(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
     CUDA_TRY(cudaStreamWaitEvent(c->xs, c->ev_fork, 0));
     intra_stream = c->aux;
-    const int rc = launch_cross(c, cross, {}, c->xs, split_ctas);
+    const int rc = launch_cross(c, cross, c->xs, split_ctas);
     if (rc != RP_OK) return rc;
     CUDA_TRY(cudaEventRecord(c->ev_xjoin, c->xs));
   }
@@ -381,7 +399,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     if (rc != RP_OK) return fail(rc, err);
     if (timing) {
       CUDA_TRY(cudaEventRecord(e1, intra_stream));
-      c->timed.push_back({e0, e1, bytes, 0, false});
+      c->timed.push_back({e0, e1, bytes, 0, false, c->batches});
     }
     c->stats.kernel_launches++;
     c->stats.bytes_hbm += bytes;
@@ -397,7 +415,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     if (rc != RP_OK) return rc;
   }
   if (!split && !cross.empty()) {
-    const int rc = launch_cross(c, cross, fused, L.stream);
+    const int rc = launch_cross(c, cross, L.stream);
     if (rc != RP_OK) return rc;
   }
   CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
@@ -413,106 +431,69 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   return RP_OK;
 }
 
-// This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch
-// (caller holds mu; members' arrival events already joined into `stream`).
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local,
-                 cudaStream_t stream, int max_ctas) {
-  if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
-  if (static_cast<int>(seqs.size()) > rp::kMaxXParts)
-    return fail(RP_EINVAL, "more than 8 cross-GPU groups on one GPU in one step");
+// Addresses of GPU d's objects as seen from this process: its flag array, the staging region of
+// its local worker `region`, and worker m's replica (all local when emulating).
+unsigned long long* flags_of(rp_ctx* c, int d) {
+  if (c->emulate) return c->vflags + static_cast<size_t>(d) * rp::kFlagWords;
+  return d == c->cfg.rank ? c->flags : c->peer_flags[d];
+}
+float* stage_of(rp_ctx* c, int d, int region) {
+  char* base = c->emulate ? reinterpret_cast<char*>(c->vstage) + static_cast<int64_t>(d) * c->cfg.workers_per_gpu *
+                                                                    c->stage_region
+                          : reinterpret_cast<char*>(d == c->cfg.rank ? c->stage : c->peer_stage[d]);
+  return base ? reinterpret_cast<float*>(base + region * c->stage_region) : nullptr;
+}
+float* replica_of(rp_ctx* c, int m) {
+  return c->emulate || c->w[m].local ? c->w[m].x : c->peer_x[m];
+}
+
+// GPU `gpu`'s parts of the cross-GPU groups `seqs` (ascending seq: the same part order on every
+// GPU), with the algorithmic bytes of those parts (caller holds mu).
+int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, int gpu, rp::XTask& T, int64_t* nvl_out,
+               int64_t* hbm_out) {
   const int wpg = c->cfg.workers_per_gpu;
-  rp::XTask T{};
-  T.nparts = static_cast<int32_t>(seqs.size());
-  T.my_gpu = c->cfg.rank;
+  T = rp::XTask{};
+  T.my_gpu = gpu;
   T.n = c->cfg.n_params;
-  T.my_flags = c->flags;
-  T.max_ctas = max_ctas;
+  T.my_flags = flags_of(c, gpu);
   T.bf16 = c->cfg.dtype == RP_DTYPE_BF16;
+  T.watchdog_ns = c->watchdog_ns;
+  T.err = c->xerr_dev;
   const int64_t esz = T.bf16 ? 2 : 4;  // bytes per replica element
-  for (size_t pi = 0; pi < seqs.size(); ++pi) {
-    ActiveGroup& a = c->active.at(seqs[pi]);
-    rp::XPart& p = T.part[pi];
+  int64_t nvl = 0, hbm = 0;
+  for (int64_t q : seqs) {
+    ActiveGroup& a = c->active.at(q);
+    if (!((gpu_mask(c, a.g) >> gpu) & 1)) continue;
+    if (T.nparts >= rp::kMaxXParts) return fail(RP_EINVAL, "more than 8 cross-GPU groups on one GPU in one step");
+    rp::XPart& p = T.part[T.nparts++];
     p.k_total = a.g.size;
     p.slot = a.g.members[0];
-    p.tag = a.g.seq >= 0 ? static_cast<uint64_t>(a.g.seq) + 1 : static_cast<uint64_t>(a.g.seq);
     int last_gpu = -1;
     for (int i = 0; i < a.g.size; ++i) {
       const int m = a.g.members[i];
-      const int gpu = m / wpg;
-      if (gpu != last_gpu) {  // first (lowest) member on this GPU: receives the means, owns the region
+      const int d = m / wpg;
+      if (d != last_gpu) {  // first (lowest) member on GPU d: receives the means, owns the region
         if (p.kp >= rp::kMaxXGpus) return fail(RP_EINVAL, "group spans more than 8 GPUs");
-        const int region = m - gpu * wpg;
-        p.gpu[p.kp] = gpu;
-        if (gpu == c->cfg.rank) {
-          p.me = p.kp;
-          p.xfirst[p.kp] = c->w[m].x;
-          p.stage[p.kp] = reinterpret_cast<float*>(reinterpret_cast<char*>(c->stage) + region * c->stage_region);
-          p.pflags[p.kp] = c->flags;
-        } else {
-          p.xfirst[p.kp] = c->peer_x[m];
-          p.stage[p.kp] =
-              reinterpret_cast<float*>(reinterpret_cast<char*>(c->peer_stage[gpu]) + region * c->stage_region);
-          p.pflags[p.kp] = c->peer_flags[gpu];
-        }
+        p.gpu[p.kp] = d;
+        if (d == gpu) p.me = p.kp;
+        p.xfirst[p.kp] = replica_of(c, m);
+        p.stage[p.kp] = stage_of(c, d, m - d * wpg);
+        p.pflags[p.kp] = flags_of(c, d);
         p.kp++;
-        last_gpu = gpu;
+        last_gpu = d;
       }
-      if (gpu == c->cfg.rank) {
+      if (d == gpu) {
         if (p.m >= rp::kMaxXLocal) return fail(RP_EINVAL, "more than 8 local members in a cross-GPU group");
         p.x[p.m] = c->w[m].x;
         p.u[p.m] = a.u[i];
         p.m++;
       }
     }
+    for (int d = 0; d < p.kp; ++d)
+      if (d != p.me) p.tag[d] = ++c->pair_tag[gpu][p.slot][p.gpu[d]];
     rp::xgpu_geometry(p, T.n);
-    c->stats.groups_launched++;
-    c->stats.cross_gpu_groups++;
-  }
-  int64_t hbm_local = 0;
-  for (int64_t q : local) {  // fused intra-GPU groups (L items)
-    ActiveGroup& a = c->active.at(q);
-    rp::XLocalGroup& G = T.lg[T.nlocal++];
-    G.k = a.g.size;
-    for (int i = 0; i < a.g.size; ++i) {
-      G.x[i] = c->w[a.g.members[i]].x;
-      G.u[i] = a.u[i];
-      hbm_local += member_bytes(a.u[i]) * T.n;
-    }
-    c->stats.groups_launched++;
-    if (a.g.size == 1) c->stats.singleton_groups++;
-  }
-  const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing) {
-    e0 = timing_event(c);
-    e1 = timing_event(c);
-    if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
-    CUDA_TRY(cudaEventRecord(e0, stream));
-  }
-  if (!c->prof_path.empty()) {
-    int64_t items = 0;
-    // upper bound: chunks per slice <= kMaxChunks, per local group <= resident CTAs + 1
-    for (int pi = 0; pi < T.nparts; ++pi) items += (2 * T.part[pi].kp - 1) * static_cast<int64_t>(rp::kMaxChunks);
-    items += static_cast<int64_t>(T.nlocal) * 4096;
-    if (items > c->prof_cap) {
-      if (c->prof) cudaFree(c->prof);
-      c->prof = nullptr;
-      c->prof_cap = 0;
-      if (cudaMalloc(&c->prof, items * sizeof(rp::XItemRecord)) == cudaSuccess) c->prof_cap = items;
-    }
-    T.prof = c->prof;
-    c->prof_items = items;
-    if (c->prof) cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
-  }
-  std::string err;
-  const int rc = rp::launch_xgpu(T, stream, &err);
-  if (rc != RP_OK) return fail(rc, err);
-  // algorithmic bytes of this GPU's parts: NVLink bytes this GPU stores into peers
-  // (A: its partials of the other slices; B: its slice's means to every peer)
-  // (fp32 partials are staged and pushed as fp32; bf16 replicas move esz = 2 bytes per element)
-  int64_t nvl = 0, hbm = 0;
-  for (int pi = 0; pi < T.nparts; ++pi) {
-    const rp::XPart& p = T.part[pi];
+    // NVLink bytes this GPU stores into peers: A, its partials of the other slices; B, its
+    // slice's means to every peer (fp32 partials; bf16 replicas move esz = 2 bytes per element)
     const int64_t lo = std::min<int64_t>(p.me * p.S4, p.n4), hi = std::min<int64_t>((p.me + 1) * p.S4, p.n4);
     int64_t mine = 4 * (hi - lo);
     if (p.me == p.kp - 1) mine += p.rem;
@@ -523,10 +504,65 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<
     // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
     hbm += rd * T.n + 4 * (p.kp - 1) * mine + esz * p.m * mine + 2 * esz * (p.m - 1) * others;
   }
-  hbm += hbm_local;
+  *nvl_out = nvl;
+  *hbm_out = hbm;
+  return RP_OK;
+}
+
+// This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch (caller holds mu;
+// members' arrival events already joined into `stream`). Emulated GPUs: every virtual GPU's
+// parts in ONE cooperative launch.
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t stream, int max_ctas) {
+  if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
+  std::vector<int64_t> seqs(seqs_in);
+  std::sort(seqs.begin(), seqs.end());
+  c->stats.groups_launched += static_cast<int64_t>(seqs.size());
+  c->stats.cross_gpu_groups += static_cast<int64_t>(seqs.size());
+  const bool timing = (c->cfg.flags & RP_FLAG_TIMING) != 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing) {
+    e0 = timing_event(c);
+    e1 = timing_event(c);
+    if (!e0 || !e1) return fail(RP_ECUDA, "timing event creation failed");
+    CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  int64_t nvl = 0, hbm = 0;
+  std::string err;
+  if (c->emulate) {
+    const int V = c->cfg.n_gpus;
+    std::vector<rp::XTask> tasks(V);
+    for (int d = 0; d < V; ++d) {
+      int64_t a = 0, b = 0;
+      const int rc = build_task(c, seqs, d, tasks[d], &a, &b);
+      if (rc != RP_OK) return rc;
+      nvl += a;
+      hbm += b;
+    }
+    const int rc = rp::launch_xgpu_emulated(tasks.data(), V, c->d_tasks, stream, &err);
+    if (rc != RP_OK) return fail(rc, err);
+  } else {
+    rp::XTask T;
+    int rc = build_task(c, seqs, c->cfg.rank, T, &nvl, &hbm);
+    if (rc != RP_OK) return rc;
+    T.max_ctas = max_ctas;
+    if (!c->prof_path.empty()) {
+      const int64_t items = static_cast<int64_t>(T.nparts) * 3 * rp::kMaxChunks;
+      if (items > c->prof_cap) {
+        if (c->prof) cudaFree(c->prof);
+        c->prof = nullptr;
+        c->prof_cap = 0;
+        if (cudaMalloc(&c->prof, items * sizeof(rp::XItemRecord)) == cudaSuccess) c->prof_cap = items;
+      }
+      T.prof = c->prof;
+      c->prof_items = items;
+      if (c->prof) cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
+    }
+    rc = rp::launch_xgpu(T, stream, &err);
+    if (rc != RP_OK) return fail(rc, err);
+  }
   if (timing) {
     CUDA_TRY(cudaEventRecord(e1, stream));
-    c->timed.push_back({e0, e1, hbm, nvl, true});
+    c->timed.push_back({e0, e1, hbm, nvl, true, c->batches});
   }
   c->stats.kernel_launches++;
   c->stats.bytes_hbm += hbm;
@@ -570,6 +606,9 @@ int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream
     p.mc = reinterpret_cast<float*>(mcb);
     p.ucf = reinterpret_cast<unsigned long long*>(ucb + o->data_bytes);
     p.mcf = reinterpret_cast<unsigned long long*>(mcb + o->data_bytes);
+    p.watchdog_ns = c->watchdog_ns;
+    p.err = c->xerr_dev;
+    p.gpu = c->cfg.rank;
     int64_t rd = 0;
     for (int i = 0; i < a.g.size; ++i) {
       const int m = a.g.members[i];
@@ -601,7 +640,7 @@ int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream
   if (rc != RP_OK) return fail(rc, err);
   if (timing) {
     CUDA_TRY(cudaEventRecord(e1, stream));
-    c->timed.push_back({e0, e1, hbm, nvl, true});
+    c->timed.push_back({e0, e1, hbm, nvl, true, c->batches});
   }
   c->stats.kernel_launches++;
   c->stats.bytes_hbm += hbm;
@@ -618,7 +657,7 @@ int launch_cross_async(rp_ctx* c, int64_t seq) {
                                   " hold an unfinished group");
   for (int m = 0; m < RP_MAX_WORLD; ++m)
     if ((a.local_mask >> m) & 1) CUDA_TRY(cudaStreamWaitEvent(c->comm, c->w[m].ev_arrive, 0));
-  const int rc = nvls_group(c, a.g) ? launch_nvls_groups(c, {seq}, c->comm) : launch_cross(c, {seq}, {}, c->comm);
+  const int rc = nvls_group(c, a.g) ? launch_nvls_groups(c, {seq}, c->comm) : launch_cross(c, {seq}, c->comm);
   if (rc != RP_OK) return rc;
   WorkerSlot& L = c->w[__builtin_ctzll(a.local_mask)];
   CUDA_TRY(cudaEventRecord(L.ev_group, c->comm));
@@ -804,6 +843,8 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       return fail(RP_EINVAL, "rp_init: world must equal n_gpus * workers_per_gpu");
     if (k.rank < 0 || k.rank >= k.n_gpus) return fail(RP_EINVAL, "rp_init: rank out of range");
   }
+  if ((k.flags & RP_FLAG_EMULATE) && (k.n_gpus < 2 || k.rank != 0 || (k.flags & RP_FLAG_SHARED_GG)))
+    return fail(RP_EINVAL, "rp_init: RP_FLAG_EMULATE needs n_gpus >= 2 virtual GPUs, rank 0 and a private GG");
   rp_ctx* c = new (std::nothrow) rp_ctx();
   if (!c) return fail(RP_ENOMEM, "rp_init: allocation failed");
   c->cfg = k;
@@ -842,8 +883,10 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       return cuda_fail(e, "cudaSetDevice");
     }
     c->has_gpu = true;
+    c->emulate = (k.flags & RP_FLAG_EMULATE) != 0;
     const int wpg = c->cfg.workers_per_gpu;
-    for (int w = k.rank * wpg; w < (k.rank + 1) * wpg; ++w) {
+    const int w_lo = c->emulate ? 0 : k.rank * wpg, w_hi = c->emulate ? k.world : (k.rank + 1) * wpg;
+    for (int w = w_lo; w < w_hi; ++w) {
       WorkerSlot& s = c->w[w];
       s.local = true;
       if ((e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -871,11 +914,33 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
         return fail(RP_EINVAL, "rp_init: at most 16 workers per GPU in a multi-GPU job");
       }
       c->stage_region = (rp::xgpu_stage_region_bytes(k.n_params) + 255) / 256 * 256;
-      if ((e = cudaMalloc(&c->flags, rp::kFlagWords * 8)) != cudaSuccess ||
-          (e = cudaMemset(c->flags, 0, rp::kFlagWords * 8)) != cudaSuccess ||
-          (e = cudaMalloc(&c->stage, c->stage_region * wpg)) != cudaSuccess) {
+      // flag-wait watchdog: rp_config.watchdog_s (0 = default 600 s, < 0 = off), RP_WATCHDOG_S overrides
+      double wd = k.watchdog_s == 0 ? 600.0 : (k.watchdog_s < 0 ? 0.0 : static_cast<double>(k.watchdog_s));
+      if (const char* v = std::getenv("RP_WATCHDOG_S"))
+        if (*v) wd = std::atof(v);
+      c->watchdog_ns = wd > 0 ? static_cast<unsigned long long>(wd * 1e9) : 0ull;
+      if ((e = cudaHostAlloc(reinterpret_cast<void**>(&c->xerr), sizeof(rp::XErr), cudaHostAllocMapped)) !=
+              cudaSuccess ||
+          (e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->xerr_dev), c->xerr, 0)) != cudaSuccess) {
+        rp_finalize(c);
+        return cuda_fail(e, "rp_init: watchdog record");
+      }
+      std::memset(c->xerr, 0, sizeof(rp::XErr));
+      const int nflag = c->emulate ? k.n_gpus : 1;
+      if ((e = cudaMalloc(&c->flags, rp::kFlagWords * 8 * nflag)) != cudaSuccess ||
+          (e = cudaMemset(c->flags, 0, rp::kFlagWords * 8 * nflag)) != cudaSuccess ||
+          (e = cudaMalloc(&c->stage, c->stage_region * wpg * nflag)) != cudaSuccess) {
         rp_finalize(c);
         return cuda_fail(e, "rp_init: flag buffers");
+      }
+      if (c->emulate) {  // virtual GPU d: flag array d, staging regions [d*wpg, (d+1)*wpg)
+        c->vflags = c->flags;
+        c->vstage = c->stage;
+        if ((e = cudaMalloc(&c->d_tasks, sizeof(rp::XTask) * k.n_gpus)) != cudaSuccess) {
+          rp_finalize(c);
+          return cuda_fail(e, "rp_init: emulation task buffer");
+        }
+        c->peers_ready = true;
       }
     }
   }
@@ -885,6 +950,7 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
 
 int rp_peer_export(rp_ctx* c, rp_peer_info* out) {
   if (!c || !out) return fail(RP_EINVAL, "null argument");
+  if (c->emulate) return fail(RP_ESTATE, "rp_peer_export: emulated GPUs share one process (RP_FLAG_EMULATE)");
   if (!c->has_gpu || c->cfg.n_gpus < 2 || !c->flags) return fail(RP_ESTATE, "rp_peer_export: not a multi-GPU context");
   std::lock_guard<std::mutex> lk(c->mu);
   cudaSetDevice(c->cfg.device);
@@ -917,6 +983,7 @@ int rp_peer_export(rp_ctx* c, rp_peer_info* out) {
 
 int rp_peer_import(rp_ctx* c, const rp_peer_info* infos, int32_t n) {
   if (!c || !infos) return fail(RP_EINVAL, "null argument");
+  if (c->emulate) return fail(RP_ESTATE, "rp_peer_import: emulated GPUs share one process (RP_FLAG_EMULATE)");
   if (!c->has_gpu || c->cfg.n_gpus < 2 || !c->flags) return fail(RP_ESTATE, "rp_peer_import: not a multi-GPU context");
   if (n != c->cfg.n_gpus) return fail(RP_EINVAL, "rp_peer_import: need one record per GPU");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1019,6 +1086,7 @@ int rp_finalize(rp_ctx* c) {
       cudaStreamSynchronize(c->xs);
       cudaStreamDestroy(c->xs);
     }
+    cudaDeviceSynchronize();  // no kernel may still use the peer mappings closed below
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_xjoin) cudaEventDestroy(c->ev_xjoin);
@@ -1027,6 +1095,8 @@ int rp_finalize(rp_ctx* c) {
     rp::nvls_teardown(&c->nvls);
     if (c->flags) cudaFree(c->flags);
     if (c->stage) cudaFree(c->stage);
+    if (c->d_tasks) cudaFree(c->d_tasks);
+    if (c->xerr) cudaFreeHost(c->xerr);
     if (c->prof) {
       // dump the item timeline of the last cross-GPU launch
       std::vector<rp::XItemRecord> h(c->prof_items);
@@ -1280,7 +1350,7 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
     a.members_mask = mask;
     const int wpg = c->cfg.workers_per_gpu;
     for (int i = 0; i < g->size; ++i)
-      if (g->members[i] / wpg == c->cfg.rank) a.local_mask |= 1ull << g->members[i];
+      if (c->emulate || g->members[i] / wpg == c->cfg.rank) a.local_mask |= 1ull << g->members[i];
     it = c->active.emplace(g->seq, a).first;
   } else if (!same_group(it->second.g, *g)) {
     return fail(RP_EPROTO, "rp_preduce: members disagree on group " + std::to_string(g->seq) + ": " +
@@ -1288,7 +1358,7 @@ int rp_preduce(rp_ctx* c, int32_t w, const rp_group* g) {
   }
   ActiveGroup& a = it->second;
   if ((a.arrived >> w) & 1) return fail(RP_EPROTO, "rp_preduce: worker arrived twice");
-  if (a.local_mask != a.members_mask && !c->batching && !(c->shm && g->seq >= 0))
+  if (is_cross(c, a) && !c->batching && !(c->shm && g->seq >= 0 && !c->emulate))
     return fail(RP_ESTATE, "rp_preduce: a cross-GPU group must be issued inside rp_batch_begin/end "
                            "(one launch per GPU and step keeps the GPUs' launch orders consistent), "
                            "or be a shared-GG group (RP_FLAG_SHARED_GG)");
@@ -1356,6 +1426,8 @@ int rp_barrier_free_wait(rp_ctx* c, int32_t w, int64_t timeout_us) {
       std::this_thread::yield();
     }
     lk.lock();
+    const int xrc = check_xerr(c);
+    if (xrc != RP_OK) return xrc;
   }
   ActiveGroup& a = c->active.at(seq);
   s.in_group = false;
@@ -1394,7 +1466,23 @@ int rp_batch_end(rp_ctx* c) {
   cudaSetDevice(c->cfg.device);
   std::vector<int64_t> q;
   q.swap(c->ready);
-  return launch_groups(c, q);
+  const int rc = launch_groups(c, q);
+  c->batches++;
+  return rc;
+}
+
+int rp_set_compute_delay(rp_ctx* c, int32_t w, int64_t ns) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  if (!c->has_gpu) return fail(RP_ENODEV, "host-only context");
+  if (!worker_ok(c, w) || !c->w[w].local || ns < 0) return fail(RP_EINVAL, "rp_set_compute_delay: bad worker or ns");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->w[w].delay_ns = ns;
+  return RP_OK;
+}
+
+int rp_check(rp_ctx* c) {
+  if (!c) return fail(RP_EINVAL, "null ctx");
+  return check_xerr(c);
 }
 
 int rp_timing_read(rp_ctx* c, rp_timing* out) {
@@ -1429,6 +1517,26 @@ int rp_timing_read(rp_ctx* c, rp_timing* out) {
   }
   c->timed.clear();
   *out = r;
+  return RP_OK;
+}
+
+int rp_timing_records(rp_ctx* c, rp_launch_record* out, int32_t cap, int32_t* n) {
+  if (!c || !n || cap < 0 || (cap > 0 && !out)) return fail(RP_EINVAL, "bad argument");
+  if (!(c->cfg.flags & RP_FLAG_TIMING)) return fail(RP_ESTATE, "context created without RP_FLAG_TIMING");
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaSetDevice(c->cfg.device);
+  const size_t k = std::min<size_t>(static_cast<size_t>(cap), c->timed.size());
+  for (size_t i = 0; i < k; ++i) {
+    auto& t = c->timed[i];
+    CUDA_TRY(cudaEventSynchronize(t.stop));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, t.start, t.stop));
+    out[i] = rp_launch_record{ms, t.bytes_hbm, t.bytes_nvlink, t.batch, t.cross ? 1 : 0, 0};
+    c->event_pool.push_back(t.start);
+    c->event_pool.push_back(t.stop);
+  }
+  c->timed.erase(c->timed.begin(), c->timed.begin() + static_cast<std::ptrdiff_t>(k));
+  *n = static_cast<int32_t>(k);
   return RP_OK;
 }
 
@@ -1489,7 +1597,14 @@ int rp_lockstep_run(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr
   std::vector<int64_t> foreign;
   for (int64_t s = 0; s < steps; ++s) {
     const int64_t t = t0 + s;
-    for (int32_t w : local) {  // alg1 step 2 with the bound gradient
+    const int xrc = check_xerr(c);  // a cross-GPU wait of an earlier (completed) launch gave up
+    if (xrc != RP_OK) return xrc;
+    for (int32_t w : local) {  // synthetic compute (harness), then alg1 step 2 with the bound gradient
+      if (c->w[w].delay_ns > 0) {
+        std::string err;
+        const int drc = rp::launch_delay(c->w[w].stream, c->w[w].delay_ns, &err);
+        if (drc != RP_OK) return fail(drc, err);
+      }
       const int rc = stage_step(c, w, nullptr, lr);
       if (rc != RP_OK) return rc;
     }

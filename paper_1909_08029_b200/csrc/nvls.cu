@@ -77,20 +77,34 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-// Watchdog: a peer that never posts its flag (a crashed rank, a broken collective contract)
-// traps the kernel after kWaitTrapNs instead of spinning forever, so the process fails with a
-// CUDA error rather than hanging the GPU. The clock is read once per 4096 polls.
-constexpr unsigned long long kWaitTrapNs = 30ull * 1000 * 1000 * 1000;
-__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long tag) {
+// Watchdog: a peer that never posts its flag (a crashed rank, a broken collective contract) ends
+// the wait after p.watchdog_ns (rp_config.watchdog_s / RP_WATCHDOG_S; 0 = wait forever): the flag
+// is recorded in host-mapped memory (the host reports RP_ETIMEOUT) and every later wait of the
+// job returns at once, so the kernel finishes (with garbage) instead of hanging the GPU.
+__device__ __noinline__ void wait_flag(const NPart& p, const unsigned long long* f, unsigned long long tag, int kind,
+                                       int64_t c) {
   if (ld_acquire_sys(f) == tag) return;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
   for (unsigned n = 1; ld_acquire_sys(f) != tag; ++n) {
     __nanosleep(32);
-    if ((n & 4095u) == 0) {
+    if (p.watchdog_ns && (n & 1023u) == 0) {
+      if (p.err && *reinterpret_cast<volatile unsigned long long*>(&p.err->code)) return;  // job already failed
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      if (t - t0 > kWaitTrapNs) __trap();
+      if (t - t0 > p.watchdog_ns) {
+        if (p.err && atomicCAS(&p.err->code, 0ull, 1ull) == 0ull) {
+          p.err->gpu = p.gpu;
+          p.err->src = -1;
+          p.err->kind = 16 + kind;  // NVLS flag kinds
+          p.err->slot = -1;
+          p.err->chunk = c;
+          p.err->tag = tag;
+          p.err->seen = ld_acquire_sys(f);
+          __threadfence_system();
+        }
+        return;
+      }
     }
   }
 }
@@ -146,8 +160,9 @@ __device__ __forceinline__ void post(unsigned long long* mcf, int64_t idx, unsig
     mm_st_release_u64(mcf + idx, tag);
   }
 }
-__device__ __forceinline__ void await(const unsigned long long* ucf, int64_t idx, unsigned long long tag) {
-  if (threadIdx.x == 0) wait_flag(ucf + idx, tag);
+__device__ __forceinline__ void await(const NPart& p, const unsigned long long* ucf, int64_t idx, unsigned long long tag,
+                                      int64_t c) {
+  if (threadIdx.x == 0) wait_flag(p, ucf + idx, tag, 1, c);
   __syncthreads();
 }
 
@@ -177,7 +192,7 @@ __device__ void item_P(const NPart& p, int64_t c) {
 template <int M>
 __device__ void item_R(const NPart& p, int64_t c) {
   if (threadIdx.x == 0)
-    for (int d = 0; d < p.kp; ++d) wait_flag(p.ucf + fl_arrive(c, d), p.tag);
+    for (int d = 0; d < p.kp; ++d) wait_flag(p, p.ucf + fl_arrive(c, d), p.tag, 0, c);
   __syncthreads();
   const int64_t lo = c * p.CH, hi = min(lo + p.CH, p.n4);
   const float kf = static_cast<float>(p.k_total);
@@ -199,7 +214,7 @@ __device__ void item_R(const NPart& p, int64_t c) {
 
 template <int M>
 __device__ void item_S(const NPart& p, int64_t c) {
-  await(p.ucf, fl_done(c), p.tag);
+  await(p, p.ucf, fl_done(c), p.tag, c);
   const int64_t lo = c * p.CH, hi = min(lo + p.CH, p.n4);
   for (int64_t t0 = lo; t0 < hi; t0 += kNThreads * kNU) {
     float4 v[kNU];

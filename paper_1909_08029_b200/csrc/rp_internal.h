@@ -120,9 +120,9 @@ struct XPart {
   int32_t kp;         // GPUs in the group
   int32_t me;         // this GPU's index among them (ascending GPU id)
   int32_t k_total;    // |G|
-  int32_t slot;       // flag slot
+  int32_t slot;       // flag slot (lowest member of the group)
   int32_t rem;        // n mod 4
-  uint64_t tag;       // nonzero, unique per group
+  uint64_t tag[kMaxXGpus];   // per peer: nonzero, unique per (group launch, GPU pair)
   int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry)
   float* x[kMaxXLocal];
   MemberUpdate u[kMaxXLocal];
@@ -132,20 +132,18 @@ struct XPart {
   int32_t gpu[kMaxXGpus];                 // GPU ids, ascending
 };
 
-// Optional per-item timeline (RP_XGPU_PROFILE): 4 x u64 per item.
+// Optional per-item timeline (RP_XGPU_PROFILE): 4 x u64 per item (A, B, C stage of a chunk).
 struct XItemRecord {
-  unsigned long long t_start, t_ready, t_end;  // %globaltimer ns: begin, wait satisfied, flag posted
+  unsigned long long t_start, t_ready, t_end;  // %globaltimer ns: begin, wait satisfied, end
   unsigned long long meta;                     // kind (2 bits) | part (6) | cta (24) | chunk (32)
 };
 
-// Intra-GPU groups of the same step fused into the cross-GPU launch ("L items"),
-// so their HBM-only work overlaps the NVLink transfers.
-constexpr int kMaxXLocalGroups = 16;
-constexpr int kMaxFusedK = 4;
-struct XLocalGroup {
-  int32_t k;
-  float* x[kMaxFusedK];
-  MemberUpdate u[kMaxFusedK];
+// A flag wait that passed the watchdog limit (host-mapped; first failure wins).
+struct XErr {
+  unsigned long long code;  // 0 = none, 1 = flag wait timed out
+  int32_t gpu, src, kind, slot;
+  int64_t chunk;
+  unsigned long long tag, seen;
 };
 
 // Kernel parameters exceed 4 KB: CUDA >= 12.1 large-parameter launches (sm_70+).
@@ -153,26 +151,26 @@ struct XTask {
   int32_t nparts;
   int32_t my_gpu;
   int64_t n;
-  // work items (filled by the launcher): items[q] = kind << 30 | part << 27 | index,
-  // ordered so that B items of chunk c come one CTA round after its A items
-  const uint32_t* items;
-  int64_t total_items;
-  int64_t chl, nchl;                       // L items: chunk (float4) and chunks per local group
   unsigned long long* my_flags;
   int32_t max_ctas;                        // grid cap (0 = every resident CTA slot)
   int32_t bf16;                            // replicas / gradients are bf16 (reading R26)
-  XItemRecord* prof;                       // nullptr unless profiling; indexed by item
-  int32_t nlocal;
-  XLocalGroup lg[kMaxXLocalGroups];
+  XItemRecord* prof;                       // nullptr unless profiling; [part][kind][chunk]
+  unsigned long long watchdog_ns;          // flag-wait limit, 0 = wait forever
+  XErr* err;                               // host-mapped error record (device address)
   XPart part[kMaxXParts];
 };
 
-// Slice and chunk geometry of a part (kp set) for n elements.
+// Lanes of the cross-GPU kernel (chunk c runs on lane c mod kXLanes on every GPU).
+constexpr int kXLanes = 296;
+// Slice and chunk geometry of a part (kp set) for n elements (depends on n and kp only).
 void xgpu_geometry(XPart& p, int64_t n);
 // Bytes of one staging region (one cross-GPU group owned by one local worker).
 int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
+// RP_FLAG_EMULATE: the tasks of V virtual GPUs (one device) in ONE cooperative launch;
+// d_tasks: device buffer of V XTask (uploaded on `stream` before the launch).
+int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std::string* err);
 
 // ---- NVLS P-Reduce (nvls.cu kernel, nvls_setup.cpp multicast objects) ---------------------
 // One multicast object per GPU subset (mask of GPU ids, >= min_gpus GPUs), bound on every GPU
@@ -216,6 +214,9 @@ struct NPart {
   float* mc;                     // slot data, multicast address
   unsigned long long* ucf;       // slot flags, unicast
   unsigned long long* mcf;       // slot flags, multicast
+  unsigned long long watchdog_ns;  // flag-wait limit (0 = forever); a timeout is recorded in err
+  XErr* err;                       // host-mapped error record (device address), or nullptr
+  int32_t gpu;                     // this GPU's id (error record)
 };
 struct NTask {
   int32_t nparts;

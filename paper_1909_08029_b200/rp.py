@@ -28,6 +28,7 @@ RP_FLAG_TIMING = 0x2
 RP_FLAG_SHARED_GG = 0x4
 RP_FLAG_RANDOM_GG = 0x8
 RP_FLAG_INTER_INTRA = 0x10
+RP_FLAG_EMULATE = 0x20
 RP_DTYPE_F32 = 0
 RP_DTYPE_BF16 = 1
 RP_SCHED_PAPER4 = 1
@@ -57,7 +58,8 @@ class rp_config(ctypes.Structure):
         ("flags", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
         ("job_id", ctypes.c_uint64),
-        ("reserved", ctypes.c_int32 * 4),
+        ("watchdog_s", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
 
@@ -126,6 +128,17 @@ class rp_peer_info(ctypes.Structure):
     ]
 
 
+class rp_launch_record(ctypes.Structure):
+    _fields_ = [
+        ("ms", ctypes.c_double),
+        ("bytes_hbm", ctypes.c_int64),
+        ("bytes_nvlink", ctypes.c_int64),
+        ("batch", ctypes.c_int64),
+        ("cross", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
 class RPError(RuntimeError):
     def __init__(self, status, func, message):
         super().__init__(f"{func} failed: status {status}: {message}")
@@ -166,6 +179,14 @@ _SIGNATURES = {
     "rp_batch_begin": (ctypes.c_int, [_CTX]),
     "rp_batch_end": (ctypes.c_int, [_CTX]),
     "rp_timing_read": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_timing)]),
+    "rp_check": (ctypes.c_int, [_CTX]),
+    "rp_set_compute_delay": (ctypes.c_int, [_CTX, ctypes.c_int32, ctypes.c_int64]),
+    "rp_timing_records": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_launch_record), ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_int32)]),
+    "rp_bench_presum": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_int64,
+                                       ctypes.c_float, _P, _P]),
+    "rp_bench_scatter_mean": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_float, ctypes.POINTER(_P),
+                                             ctypes.c_int32, _P]),
     "rp_stats_get": (ctypes.c_int, [_CTX, ctypes.POINTER(rp_stats)]),
     "rp_trace_open": (ctypes.c_int, [_CTX, ctypes.c_char_p]),
     "rp_last_error": (ctypes.c_char_p, []),
@@ -359,6 +380,40 @@ def rp_timing_read(ctx):
     return t.as_dict()
 
 
+def rp_timing_records(ctx, cap=1 << 16):
+    """Per-launch records (RP_FLAG_TIMING), oldest first; drops them from the context."""
+    arr = (rp_launch_record * cap)()
+    n = ctypes.c_int32()
+    _check(load_library().rp_timing_records(ctx, arr, cap, ctypes.byref(n)), "rp_timing_records")
+    return [{"ms": r.ms, "bytes_hbm": r.bytes_hbm, "bytes_nvlink": r.bytes_nvlink, "batch": r.batch,
+             "cross": bool(r.cross)} for r in arr[:n.value]]
+
+
+def rp_bench_presum(xs, gs, n, lr, out, stream=0):
+    """NCCL-baseline helper: out = left fold of fl(x_i - fl(lr g_i)) (not the method's path)."""
+    m = len(xs)
+    X = (_P * m)(*[_ptr(v).value for v in xs])
+    G = (_P * m)(*[_ptr(v).value for v in gs])
+    _check(load_library().rp_bench_presum(X, G, m, n, ctypes.c_float(lr), _ptr(out), _ptr(stream)),
+           "rp_bench_presum")
+
+
+def rp_bench_scatter_mean(s, n, k, xs, stream=0):
+    """NCCL-baseline helper: x_i = fl(s / k) for every member (not the method's path)."""
+    m = len(xs)
+    X = (_P * m)(*[_ptr(v).value for v in xs])
+    _check(load_library().rp_bench_scatter_mean(_ptr(s), n, ctypes.c_float(k), X, m, _ptr(stream)),
+           "rp_bench_scatter_mean")
+
+
+def rp_set_compute_delay(ctx, w, ns):
+    _check(load_library().rp_set_compute_delay(ctx, w, int(ns)), "rp_set_compute_delay")
+
+
+def rp_check(ctx):
+    _check(load_library().rp_check(ctx), "rp_check")
+
+
 def rp_stats_get(ctx):
     s = rp_stats()
     _check(load_library().rp_stats_get(ctx, ctypes.byref(s)), "rp_stats_get")
@@ -387,7 +442,7 @@ class Context:
     """Owns one rp_ctx. Methods map 1:1 onto the C calls."""
 
     def __init__(self, world, n_params, *, n_gpus=1, workers_per_gpu=None, rank=0, device=None,
-                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0, job_id=0, dtype="f32"):
+                 group_size=2, c_thres=4, nodes=0, seed_gd=3, flags=0, job_id=0, dtype="f32", watchdog_s=0):
         if dtype not in ("f32", "bf16"):
             raise ValueError("dtype must be 'f32' or 'bf16'")
         cfg = rp_config()
@@ -405,7 +460,9 @@ class Context:
         cfg.seed_gd = seed_gd
         cfg.flags = flags
         cfg.job_id = job_id
+        cfg.watchdog_s = watchdog_s
         self.cfg = cfg
+        self.emulate = bool(flags & RP_FLAG_EMULATE)
         self.world = world
         self.n_params = n_params
         self.wpg = cfg.workers_per_gpu
@@ -413,6 +470,8 @@ class Context:
         self.handle = rp_init(cfg)
 
     def local_workers(self):
+        if self.emulate:               # every virtual GPU's workers live in this process
+            return list(range(self.world))
         return list(range(self.rank * self.wpg, (self.rank + 1) * self.wpg))
 
     def close(self):
@@ -524,6 +583,15 @@ class Context:
 
     def timing_read(self):
         return rp_timing_read(self.handle)
+
+    def check(self):
+        rp_check(self.handle)
+
+    def set_compute_delay(self, w, ns):
+        rp_set_compute_delay(self.handle, w, ns)
+
+    def timing_records(self):
+        return rp_timing_records(self.handle)
 
     def stats(self):
         return rp_stats_get(self.handle)

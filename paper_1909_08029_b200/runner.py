@@ -33,7 +33,7 @@ def _ceil_to(v, m):
 class LockstepRunner:
     def __init__(self, world, n_params, *, mode, rule=None, group_size=2, n_gpus=1, rank=0, device=None,
                  lr=0.1, c_thres=4, seed_gd=3, nodes=0, grad_mode="per_step", flags=0, init=True,
-                 peer_group=None, section_length=1, momentum=None, nvls=0, dtype="f32"):
+                 peer_group=None, section_length=1, momentum=None, nvls=0, dtype="f32", emulate=False):
         if mode not in ("static", "gd"):
             raise ValueError("mode must be 'static' or 'gd'")
         if mode == "static" and rule not in RULES:
@@ -48,6 +48,11 @@ class LockstepRunner:
         self.world, self.n = world, n_params
         self.n_gpus, self.peer_group = n_gpus, peer_group
         self.dtype = dtype                                    # "bf16": bf16 replicas (reading R26)
+        # emulate: n_gpus VIRTUAL GPUs on this one device, every worker driven by this process
+        # (RP_FLAG_EMULATE; the cross-GPU kernel of every virtual GPU in one cooperative launch)
+        self.emulate = bool(emulate)
+        if self.emulate:
+            flags |= rp.RP_FLAG_EMULATE
         self.ctx = Context(world, n_params, n_gpus=n_gpus, rank=rank, device=self.device,
                            group_size=group_size, c_thres=c_thres, nodes=nodes, seed_gd=seed_gd, flags=flags,
                            dtype=dtype)
@@ -66,7 +71,7 @@ class LockstepRunner:
         for i, w in enumerate(self.local):
             self.ctx.bind_worker(w, self.x(w), self.g(w))
             self.streams[w] = self.ctx.worker_stream(w)
-        if n_gpus > 1:
+        if n_gpus > 1 and not self.emulate:
             # map the peers' replicas + flag arrays (CUDA IPC records exchanged over
             # torch.distributed; the data path is the library's NVLink kernel)
             self.ctx.peer_setup(peer_group)
@@ -179,7 +184,7 @@ class LockstepRunner:
 
     def close(self):
         self.synchronize()
-        if self.n_gpus > 1:
+        if self.n_gpus > 1 and not self.emulate:
             # every rank's last kernel has seen its peers finish reading; the barrier keeps a
             # rank from freeing replicas another rank still has mapped
             import torch.distributed as dist

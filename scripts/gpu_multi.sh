@@ -1,15 +1,11 @@
 #!/bin/bash
-# Multi-GPU gpurun call: parity tests over NVLink, benches at N GPUs, NCCL baseline.
-# Usage: bash scripts/gpu_multi.sh TAG N
-TAG=${1:-m01}
-N=${2:-2}
-OUT=gpurun_out/$TAG
-mkdir -p $OUT
-nvidia-smi topo -m > $OUT/topo.txt 2>&1
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29533"
-timeout 1200 python -m pytest tests/test_gpu_multi.py -x -q -p no:cacheprovider > $OUT/pytest_multi.log 2>&1; echo "rc=$?" >> $OUT/pytest_multi.log
-for WL in cfg3 cfg2 cfg4; do
-  timeout 300 $TR bench.py --gpus $N --steps 50 --warmup 5 --workload $WL > $OUT/bench_${WL}.json 2> $OUT/bench_${WL}.err; echo "rc=$?" >> $OUT/bench_${WL}.err
-  timeout 300 $TR bench.py --gpus $N --steps 50 --warmup 5 --workload $WL --impl nccl > $OUT/nccl_${WL}.json 2> $OUT/nccl_${WL}.err; echo "rc=$?" >> $OUT/nccl_${WL}.err
+# bash scripts/gpu_multi.sh TAG N "workload ..." [extra bench args]: N-GPU bench lines (ours + NCCL AR)
+# for each workload, into gpurun_out/TAG/. Used from gpurun (--gpus N).
+TAG=$1; N=$2; WLS=$3; shift 3
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+T="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29541"
+for wl in $WLS; do
+  timeout 300 $T bench.py --gpus $N --workload $wl "$@" > $OUT/ours_${wl}_n$N.json 2> $OUT/ours_${wl}_n$N.err
+  timeout 300 $T bench.py --gpus $N --workload $wl --impl nccl "$@" > $OUT/ar_${wl}_n$N.json 2> $OUT/ar_${wl}_n$N.err
 done
 echo done > $OUT/DONE

@@ -1,0 +1,93 @@
+"""Cross-GPU parity on ONE GPU: RP_FLAG_EMULATE runs the cross-GPU kernel of every virtual GPU
+(flags, staging, owner slices, per-GPU partial fold, NVLink-style pushes between the virtual GPUs'
+buffers) in one cooperative launch, compared bit for bit with the oracle run with
+workers_per_gpu < world (reading R1: per-GPU partials folded in ascending GPU id).
+
+The multi-process cases (tests/test_gpu_multi.py) need >= 2 GPUs; these run on any B200.
+alg1 step 4, concurrent disjoint groups.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import sim
+
+pytestmark = pytest.mark.gpu
+
+N_R50 = 25_557_032
+
+CASES = [
+    # (V virtual GPUs, wpg, n, k, mode, rule, steps, extra)
+    (2, 1, (1 << 18) + 3, 2, "static", "shift_k", 12, {}),            # one cross pair per step, ragged tail
+    (2, 2, 100_003, 3, "static", "shift_k", 10, {}),                  # co-resident pre-reduction (m = 2)
+    (3, 1, 200_003, 3, "gd", None, 10, {}),                           # kp = 3 (configs[2] shape)
+    (4, 1, 200_003, 3, "gd", None, 10, {}),                           # kp <= 3 among 4 GPUs
+    (4, 2, 150_001, 3, "static", "shift_k", 9, {}),                   # configs[3] shape: 2 cross parts per GPU
+    (2, 4, 100_003, 3, "gd", None, 10, {}),                           # r50x8 layout at N = 2, m up to 3
+    (4, 2, 120_011, 4, "static", "paper4", 8, {}),                    # PAPER4 4 nodes x 2, kp = 4
+    (4, 1, 3_000_017, 4, "static", "shift_k", 4, {}),                 # multi-chunk lanes (nch > lanes), kp = 4
+    (2, 1, 5, 2, "static", "shift_k", 6, {}),                         # slices smaller than a tile
+    (2, 1, 1, 2, "static", "shift_k", 4, {}),                         # scalar only (empty vector slices)
+    (8, 1, 100_003, 8, "static", "shift_k", 4, {}),                   # kp = 8: one group of all GPUs
+    (2, 2, 100_003, 3, "static", "shift_k", 8, {"dtype": "bf16"}),    # bf16 replicas (R26)
+    (4, 1, 200_003, 3, "gd", None, 8, {"dtype": "bf16"}),
+    (2, 1, 4102, 2, "static", "shift_k", 6, {"dtype": "bf16"}),       # odd bf16 vector count
+    (2, 2, 60_011, 3, "static", "shift_k", 8, {"momentum": (0.9, 1e-4)}),
+    (2, 4, 30_001, 3, "gd", None, 9, {"momentum": (0.9, 1e-4), "section_length": 2}),
+    (2, 4, 50_007, 3, "gd", None, 8, {"ii": True}),                   # Inter-Intra (§5.2)
+    (2, 4, 100_003, 3, "gd", None, 12, {"native": True}),             # rp_lockstep_run, resident grads
+    (4, 2, 200_003, 3, "gd", None, 10, {"native": True}),
+]
+
+
+def _run(V, wpg, n, k, mode, rule, steps, extra, sample=0):
+    import paper_1909_08029_b200 as rp
+    from paper_1909_08029_b200.runner import LockstepRunner
+    world = V * wpg
+    ii = extra.get("ii", False)
+    nodes = V if (rule == "paper4" or ii) else 0
+    native = extra.get("native", False)
+    mom = extra.get("momentum")
+    dtype = extra.get("dtype", "f32")
+    L = extra.get("section_length", 1)
+    r = LockstepRunner(world, n, mode=mode, rule=rule, group_size=k, n_gpus=V, device=0, nodes=nodes,
+                       flags=rp.RP_FLAG_INTER_INTRA if ii else 0, momentum=mom, section_length=L, dtype=dtype,
+                       grad_mode="resident" if native else "per_step", emulate=True)
+    if native:
+        r.run_native(steps)
+        log = None
+    else:
+        log = r.run(steps)
+    r.synchronize()
+    slices = [(0, n)] if not sample else [(0, sample), (n // 2, n // 2 + sample), (n - sample, n)]
+    for lo, hi in slices:
+        X, olog = sim.run_lockstep(world, n, steps, mode=mode, rule=rule, k=k, nodes=nodes or None,
+                                   m=(world // nodes if nodes else None), workers_per_gpu=wpg, lo=lo, hi=hi,
+                                   ii_nodes=V if ii else 0, momentum=mom, section_length=L, dtype=dtype,
+                                   grad_step=1 if native else None)
+        for w in range(world):
+            got = r.x(w)[lo:hi].float().cpu().numpy()
+            diff = np.flatnonzero(got.view(np.uint32) != X[w].view(np.uint32))
+            assert diff.size == 0, (f"worker {w} slice [{lo},{hi}): {diff.size} elements differ, first {diff[:5]}, "
+                                    f"max abs {np.max(np.abs(got - X[w]))}")
+    if log is not None:
+        assert sorted(g for _, gs in log for g in gs) == sorted(tuple(g) for _, gs in olog for g in gs)
+    st = r.ctx.stats()
+    r.close()
+    return st
+
+
+@pytest.mark.parametrize("V,wpg,n,k,mode,rule,steps,extra", CASES)
+def test_emulated_cross_gpu_parity(V, wpg, n, k, mode, rule, steps, extra):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    st = _run(V, wpg, n, k, mode, rule, steps, extra)
+    if n > 1 or V > 1:
+        assert st["cross_gpu_groups"] > 0      # the cross-GPU kernel really ran
+
+
+def test_emulated_full_r50_sampled():
+    # ResNet-50 size, kp = 3 groups of configs[2] at 4 virtual GPUs, sampled slices vs the oracle
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    _run(4, 1, N_R50, 3, "gd", None, 3, {"native": True}, sample=4099)

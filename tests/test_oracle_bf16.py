@@ -43,6 +43,22 @@ def test_bf16_round_matches_torch_conversion():
     assert same.all(), x[~same][:5]
 
 
+def test_bf16_round_non_finite():
+    # reading R26: +-inf stay +-inf, every NaN (any payload, either sign) stays a NaN; before this
+    # pin the carry of the rounding turned 0xffffffff into +0.0 (found by review, round 2).
+    # torch's CPU conversion is the independent implementation for the class of each result.
+    bits = np.array([0x7F800000, 0xFF800000, 0x7FC00000, 0xFFC00000, 0x7FFFFFFF, 0xFFFFFFFF,
+                     0x7F800001, 0xFF800001, 0x7FBFFFFF, 0x7F7FFFFF], dtype=np.uint32)
+    x = bits.view(F32)
+    got = U.bf16_round(x)
+    want = torch.from_numpy(x.copy()).to(torch.bfloat16).to(torch.float32).numpy()
+    assert np.array_equal(np.isnan(got), np.isnan(x))
+    fin = ~np.isnan(x)
+    assert np.array_equal(got[fin].view(np.uint32), want[fin].view(np.uint32))   # inf, FLT_MAX -> inf
+    assert np.array_equal(np.signbit(got[~fin]), np.signbit(x[~fin]))
+    assert np.all(got.view(np.uint32) & 0xFFFF == 0)                                 # a bf16 value
+
+
 def _bf16_vecs(rng, n, N):
     return {w: U.bf16_round(rng.standard_normal(N).astype(F32)) for w in range(n)}
 
