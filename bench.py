@@ -46,8 +46,9 @@ WORKLOADS = {
                        "lockstep requests in ascending order) spread over N B200 (8/N workers per GPU): N=1 is "
                        "configs[1], N=8 is configs[2]",
                   world=8, n=N_R50, k=3, mode="gd", rule=None, scaling="strong"),
-    "cfg1": dict(desc="configs[0]: 4 workers, 1M fp32, k=2, static SHIFT_K(4,2), 1 GPU",
-                 wpg=4, n=1 << 20, k=2, mode="static", rule="shift_k"),
+    "cfg1": dict(desc="configs[0]: 4 workers, 1M fp32, k=2, static SHIFT_K(4,2), 1 GPU; one schedule period "
+                      "captured into a CUDA graph and replayed (RP_FLAG_GRAPH: launch-bound size)",
+                 wpg=4, n=1 << 20, k=2, mode="static", rule="shift_k", graph=True),
     "cfg2": dict(desc="configs[1] layout weak-scaled: 8 workers per B200, ResNet-50-sized, k=3, GB+GD over all "
                       "8*N workers (N=1: exactly configs[1])",
                  wpg=8, n=N_R50, k=3, mode="gd", rule=None),
@@ -75,6 +76,9 @@ WORKLOADS = {
                  wpg=1, n=N_R50, k=64, mode="static", rule="shift_k"),
     "xall_vgg": dict(desc="diagnostic: 1 worker per B200, VGG-16-sized, ONE group of all N GPUs every step",
                      wpg=1, n=N_VGG, k=64, mode="static", rule="shift_k"),
+    "xall_vgg_m2": dict(desc="diagnostic: 2 workers per B200, VGG-16-sized, ONE group of all 2N workers every step "
+                             "(every GPU pre-reduces 2 members: the HBM-heavy side of configs[3])",
+                        wpg=2, n=N_VGG, k=64, mode="static", rule="shift_k"),
     "cfg5": dict(desc="configs[4]: 2 workers per B200, VGG-16-sized, k=3, asynchronous GB+GD+filter (C_thres=4), "
                       "worker 0 slowed by --slow x T_c (P:1395)",
                  wpg=2, n=N_VGG, k=3, mode="async", rule=None),
@@ -322,6 +326,8 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
     world = wpg * n_gpus
     k = min(wl["k"], world)              # e.g. one group of all GPUs for xall
     flags = rp.RP_FLAG_TIMING | (rp.RP_FLAG_INTER_INTRA if wl.get("inter_intra") else 0)
+    if wl.get("graph") and n_gpus == 1 and not args.per_call:
+        flags |= rp.RP_FLAG_GRAPH
     nodes = n_gpus if (wl.get("inter_intra") or wl["rule"] == "paper4") else 0
     runner = LockstepRunner(world, n, mode=wl["mode"], rule=wl["rule"], group_size=k, n_gpus=n_gpus,
                             rank=rank, device=D.local_rank, grad_mode="resident", flags=flags, nodes=nodes,
@@ -388,6 +394,13 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
     if roof is not None:
         roof = dict(roof)
         roof["other_kernel"] = hroof if main_is_x else xroof
+    elif hbm_step > 0:        # CUDA-graph replay (RP_FLAG_GRAPH): no per-launch events, whole step
+        a = hbm_step / (ms / steps / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "whole lockstep step (CUDA graph replay of the fused SGD + P-Reduce "
+                                          "launches; per-launch events are not captured)",
+                "achieved": round(a, 1), "peak": peaks["hbm_gbs"], "peak_source": peak_src, "unit": "GB/s",
+                "frac": round(a / peaks["hbm_gbs"], 4), "frac_of_nominal": round(a / HBM_NOMINAL, 4),
+                "traffic": traffic_from_profiles(name, n_gpus), "algorithmic_bytes_per_step": int(hbm_step)}
     return {
         "metric": METRIC, "value": round(value, 1), "unit": "worker-steps/s", "n_gpus": n_gpus,
         "steps": steps, "warmup": warmup, "ms_per_step": round(ms / steps, 4), "higher_is_better": True,

@@ -80,6 +80,10 @@ extern "C" {
                                    Division queues an Inter group (Head Workers across
                                    nodes, the rest node-local) and an Intra group (whole
                                    node); nodes = cfg.nodes, or n_gpus when 0           */
+#define RP_FLAG_GRAPH 0x40      /* rp_lockstep_run with a static rule on one GPU: capture one
+                                   schedule period (lcm(4 or k, section length) steps) into
+                                   a CUDA graph once and replay it (launch-bound small
+                                   configs, e.g. configs[0]); no timing events inside   */
 #define RP_FLAG_EMULATE 0x20    /* parity tool: n_gpus VIRTUAL GPUs on one device, one
                                    process (rank 0, every worker local): cross-GPU
                                    groups run the cross-GPU kernel for every virtual GPU

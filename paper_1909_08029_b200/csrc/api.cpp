@@ -177,6 +177,7 @@ struct rp_ctx {
   float* peer_stage[RP_MAX_GPUS] = {};              // staging buffers of the other GPUs, mapped
   // optional cross-kernel item timeline (env RP_XGPU_PROFILE=path): last launch only
   rp::XItemRecord* prof = nullptr;
+  unsigned long long* cta_stat = nullptr;  // RP_XGPU_PROFILE: per-CTA wait breakdown of the last launch
   int64_t prof_cap = 0, prof_items = 0;
   std::string prof_path;
   std::vector<void*> ipc_mapped;                    // cudaIpcOpenMemHandle results
@@ -341,7 +342,20 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     const char* v = std::getenv("RP_XGPU_SPLIT");
     split_ctas = v && *v ? std::atoi(v) : 296;
   }
-  const bool split = !cross.empty() && nv.empty() && !seqs.empty() && !c->emulate && c->aux && c->xs;
+  // RP_SPLIT_ORDER (experiment): 0 = concurrent streams (default), 1 = the cross launch first and
+  // the intra-GPU launch after it on one stream, 2 = the intra-GPU launch first
+  static int split_order = -1;
+  if (split_order < 0) {
+    const char* v = std::getenv("RP_SPLIT_ORDER");
+    split_order = v && *v ? std::atoi(v) : 0;
+  }
+  const bool split = !cross.empty() && nv.empty() && !seqs.empty() && !c->emulate && c->aux && c->xs &&
+                     split_order == 0;
+  if (!split && split_order == 1 && !cross.empty() && nv.empty() && !c->emulate) {
+    const int rc = launch_cross(c, cross, L.stream);
+    if (rc != RP_OK) return rc;
+    cross.clear();
+  }
   cudaStream_t intra_stream = L.stream;
   static int tpc = -1;  // RP_DYN_TPC: tiles per CTA of the intra-GPU launch in split mode
   if (tpc < 0) {
@@ -555,7 +569,12 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
       }
       T.prof = c->prof;
       c->prof_items = items;
-      if (c->prof) cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
+      if (c->prof) {
+        cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
+        if (!c->cta_stat) cudaMalloc(&c->cta_stat, sizeof(unsigned long long) * 4 * 2048);
+        if (c->cta_stat) cudaMemsetAsync(c->cta_stat, 0, sizeof(unsigned long long) * 4 * 2048, stream);
+        T.cta_stat = c->cta_stat;
+      }
     }
     rc = rp::launch_xgpu(T, stream, &err);
     if (rc != RP_OK) return fail(rc, err);
@@ -1065,8 +1084,13 @@ int rp_nvls_enable(rp_ctx* c, int32_t min_gpus, rp_barrier_fn barrier, void* use
   return RP_OK;
 }
 
+namespace {
+void release_graph(const rp_ctx* c);
+}
+
 int rp_finalize(rp_ctx* c) {
   if (!c) return RP_OK;
+  release_graph(c);
   if (c->has_gpu) {
     cudaSetDevice(c->cfg.device);
     for (auto& t : c->timed) {
@@ -1108,6 +1132,17 @@ int rp_finalize(rp_ctx* c) {
         }
       }
       cudaFree(c->prof);
+    }
+    if (c->cta_stat) {  // per-CTA breakdown [ring wait, signal wait, flag wait, total] ns of the last launch
+      std::vector<unsigned long long> h(4 * 2048);
+      if (cudaMemcpy(h.data(), c->cta_stat, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+        const std::string path = c->prof_path + ".cta." + std::to_string(c->cfg.rank);
+        if (FILE* f = std::fopen(path.c_str(), "wb")) {
+          std::fwrite(h.data(), 8, h.size(), f);
+          std::fclose(f);
+        }
+      }
+      cudaFree(c->cta_stat);
     }
     for (auto& s : c->w) {
       if (s.stream) cudaStreamSynchronize(s.stream);
@@ -1577,12 +1612,133 @@ int rp_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uin
 
 // Native lockstep executor: the LockstepRunner's step loop (runner.py) composed from the public
 // calls above, so a lockstep step costs no per-call host overhead beyond C++.
+namespace {
+int lockstep_steps(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length);
+int lockstep_graph(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length);
+}  // namespace
+
 int rp_lockstep_run(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length) {
   if (!c) return fail(RP_EINVAL, "null ctx");
   if (!c->has_gpu) return fail(RP_ENODEV, "rp_lockstep_run: host-only context");
   if (steps < 0 || t0 < 1 || section_length < 1 ||
       (rule != RP_SCHED_GG && rule != RP_SCHED_PAPER4 && rule != RP_SCHED_SHIFT_K))
     return fail(RP_EINVAL, "rp_lockstep_run: bad rule, t0, steps or section_length");
+  bool delays = false;
+  for (int w = 0; w < c->cfg.world; ++w) delays = delays || (c->w[w].local && c->w[w].delay_ns > 0);
+  if ((c->cfg.flags & RP_FLAG_GRAPH) && rule != RP_SCHED_GG && c->cfg.n_gpus <= 1 && !delays)
+    return lockstep_graph(c, rule, t0, steps, lr, section_length);
+  return lockstep_steps(c, rule, t0, steps, lr, section_length);
+}
+
+namespace {
+
+// RP_FLAG_GRAPH: a static schedule repeats with period lcm(P, L) (P = 4 for PAPER4, k for SHIFT_K;
+// L = section length), and so does every launch of one period (kernel arguments do not depend
+// on t). One period of the native step loop is captured once into a CUDA graph (every worker
+// stream joins the capture, so the group-local event ordering is kept as graph edges) and
+// replayed; the remaining steps run through the plain loop. Host bookkeeping of a period is
+// identical every time (all groups complete within their step), so the stats are advanced by
+// the captured period's deltas. Timing events are not captured (RP_FLAG_TIMING is ignored
+// inside the graph).
+struct GraphCache {
+  int32_t rule = 0, section = 0;
+  int64_t phase = -1, period = 0;
+  uint32_t lr_bits = 0;
+  cudaGraphExec_t exec = nullptr;
+  rp_stats delta{};
+};
+std::mutex g_graph_mu;
+std::map<const rp_ctx*, GraphCache> g_graphs;
+
+int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
+
+void add_stats(rp_stats& a, const rp_stats& d, int64_t times) {
+  a.groups_launched += d.groups_launched * times;
+  a.singleton_groups += d.singleton_groups * times;
+  a.cross_gpu_groups += d.cross_gpu_groups * times;
+  a.kernel_launches += d.kernel_launches * times;
+  a.lock_assertions += d.lock_assertions * times;
+  a.bytes_hbm += d.bytes_hbm * times;
+  a.bytes_nvlink += d.bytes_nvlink * times;
+}
+
+int lockstep_graph(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length) {
+  const int64_t P = rule == RP_SCHED_PAPER4 ? 4 : std::max(1, c->cfg.group_size);
+  const int64_t period = P / gcd64(P, section_length) * section_length;
+  if (steps < period) return lockstep_steps(c, rule, t0, steps, lr, section_length);
+  std::vector<int32_t> local;
+  for (int w = 0; w < c->cfg.world; ++w)
+    if (c->w[w].local) local.push_back(w);
+  cudaStream_t s0 = c->w[local[0]].stream;
+  uint32_t lr_bits = 0;
+  std::memcpy(&lr_bits, &lr, 4);
+  std::lock_guard<std::mutex> glk(g_graph_mu);
+  GraphCache& G = g_graphs[c];
+  if (!G.exec || G.rule != rule || G.section != section_length || G.phase != t0 % period || G.lr_bits != lr_bits) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G = GraphCache{};
+    cudaSetDevice(c->cfg.device);
+    CUDA_TRY(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed));
+    // every other worker stream joins the capture through an event recorded on s0
+    int rc = RP_OK;
+    cudaError_t e = cudaEventRecord(c->w[local[0]].ev_group, s0);
+    for (size_t i = 1; i < local.size() && e == cudaSuccess; ++i)
+      e = cudaStreamWaitEvent(c->w[local[i]].stream, c->w[local[0]].ev_group, 0);
+    const rp_stats before = c->stats;
+    const int32_t saved = c->cfg.flags;
+    if (e == cudaSuccess) {
+      c->cfg.flags &= ~RP_FLAG_TIMING;
+      rc = lockstep_steps(c, rule, t0, period, lr, section_length);
+      c->cfg.flags = saved;
+    }
+    // ... and joins back: s0 waits for the last event of every other worker stream
+    for (size_t i = 1; i < local.size() && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(c->w[local[i]].ev_done, c->w[local[i]].stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, c->w[local[i]].ev_done, 0);
+    }
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(s0, &graph);
+    if (e != cudaSuccess) return cuda_fail(e, "rp_lockstep_run: graph capture");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
+    if (rc != RP_OK) {
+      cudaGraphDestroy(graph);
+      return rc;
+    }
+    e = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    G.rule = rule;
+    G.section = section_length;
+    G.phase = t0 % period;
+    G.period = period;
+    G.lr_bits = lr_bits;
+    G.delta = rp_stats{};
+    rp_stats d = c->stats;  // the capture advanced the host counters by one period
+    d.groups_launched -= before.groups_launched;
+    d.singleton_groups -= before.singleton_groups;
+    d.cross_gpu_groups -= before.cross_gpu_groups;
+    d.kernel_launches -= before.kernel_launches;
+    d.lock_assertions -= before.lock_assertions;
+    d.bytes_hbm -= before.bytes_hbm;
+    d.bytes_nvlink -= before.bytes_nvlink;
+    G.delta = d;
+    add_stats(c->stats, d, -1);  // counted again per replay below
+  }
+  const int64_t reps = steps / period;
+  for (int64_t r = 0; r < reps; ++r) CUDA_TRY(cudaGraphLaunch(G.exec, s0));
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    add_stats(c->stats, G.delta, reps);
+  }
+  // later work on any worker stream is ordered after the replays
+  CUDA_TRY(cudaEventRecord(c->w[local[0]].ev_group, s0));
+  for (size_t i = 1; i < local.size(); ++i)
+    CUDA_TRY(cudaStreamWaitEvent(c->w[local[i]].stream, c->w[local[0]].ev_group, 0));
+  const int64_t rest = steps - reps * period;
+  return rest ? lockstep_steps(c, rule, t0 + reps * period, rest, lr, section_length) : RP_OK;
+}
+
+int lockstep_steps(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr, int32_t section_length) {
   const int world = c->cfg.world;
   std::vector<int32_t> local, all(world);
   std::vector<char> is_local(world, 0);
@@ -1657,3 +1813,13 @@ int rp_lockstep_run(rp_ctx* c, int32_t rule, int64_t t0, int64_t steps, float lr
   }
   return RP_OK;
 }
+
+void release_graph(const rp_ctx* c) {
+  std::lock_guard<std::mutex> glk(g_graph_mu);
+  auto it = g_graphs.find(c);
+  if (it == g_graphs.end()) return;
+  if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+  g_graphs.erase(it);
+}
+
+}  // namespace

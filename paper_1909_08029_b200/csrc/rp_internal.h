@@ -157,6 +157,9 @@ struct XTask {
   XItemRecord* prof;                       // nullptr unless profiling; [part][kind][chunk]
   unsigned long long watchdog_ns;          // flag-wait limit, 0 = wait forever
   XErr* err;                               // host-mapped error record (device address)
+  int32_t nbuf;                            // shared-memory tile ring depth (launcher)
+  int32_t blag;                            // warp-specialized kernel: B runs blag (>= 2) iterations after A
+  unsigned long long* cta_stat;            // profiling: per CTA ns [ring wait, signal wait, flag wait, total]
   XPart part[kMaxXParts];
 };
 
@@ -168,6 +171,10 @@ void xgpu_geometry(XPart& p, int64_t n);
 int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
+// The warp-specialized cross-GPU kernel (xgpu_ws.cu; plain SGD, fp32 and bf16): TMA bulk loads
+// into a staged ring, bulk stores out. emu: d_tasks holds V uploaded tasks (cooperative launch).
+int launch_xgpu_ws(XTask& T, const XTask* d_tasks, int V, int max_parts, void* stream, std::string* err, int mmax,
+                   int kpmax, bool emu);
 // RP_FLAG_EMULATE: the tasks of V virtual GPUs (one device) in ONE cooperative launch;
 // d_tasks: device buffer of V XTask (uploaded on `stream` before the launch).
 int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std::string* err);

@@ -56,12 +56,17 @@ namespace rp {
 
 namespace {
 
+#ifndef RP_XGPU_MINB
+#define RP_XGPU_MINB 2  // resident CTAs per SM the register allocation targets
+#endif
 constexpr int kXThreads = 256;
 constexpr int kRowF4 = kXThreads;                 // vectors per tile row (one per thread)
 constexpr int kTileRows = 4;
 constexpr int64_t kTileF4 = kRowF4 * kTileRows;   // 1024 vectors: a 16 KB fp32 tile
-constexpr int kNbuf = 3;                          // shared-memory tile ring (48 KB)
-constexpr int kLaneIters = 2;                     // target pipeline iterations per lane (>= 64 KB per flag)
+constexpr int kNbufDefault = 3;                   // shared-memory tile ring (48 KB; RP_XGPU_NBUF 2..8)
+constexpr int kNbufMax = 8;
+constexpr int kLaneIters = 3;                     // target pipeline iterations per lane
+constexpr int kMinTiles = 2;                      // smallest chunk: 2 tiles (32 KB fp32)
 
 __device__ __forceinline__ float4 ldv(const float* p) {
   float4 v;
@@ -149,7 +154,11 @@ __device__ __noinline__ bool wait_flag_slow(const XTask& T, const unsigned long 
 }
 __device__ __forceinline__ bool wait_flag(const XTask& T, const unsigned long long* f, unsigned long long tag,
                                           int slot, int src, int kind, int64_t c) {
-  return ld_acquire_sys(f) == tag || wait_flag_slow(T, f, tag, slot, src, kind, c);
+  if (ld_acquire_sys(f) == tag) return true;
+  const unsigned long long t0 = T.cta_stat ? gtimer() : 0;
+  const bool ok = wait_flag_slow(T, f, tag, slot, src, kind, c);
+  if (T.cta_stat) atomicAdd(T.cta_stat + 4 * blockIdx.x + 2, gtimer() - t0);
+  return ok;
 }
 
 // ---- element access: fp32 replicas, or bf16 replicas with fp32 arithmetic (reading R26) ----
@@ -295,25 +304,45 @@ __device__ __forceinline__ int64_t stage_off(const XPart& p, int d, int64_t i_re
   return (static_cast<int64_t>(d) * (p.S4 + 1) + i_rel) * 4;
 }
 
-// Shared-memory tile ring: `slot` counts tiles issued by this CTA; a tile buffer is reused only
-// after the bulk store that read it kNbuf tiles ago has finished reading (thread 0 waits, the
-// barrier publishes). Every tile commits exactly one bulk group.
-__device__ __forceinline__ float4* acquire_tile(float4* smem, int& slot) {
-  if (threadIdx.x == 0) bulk_wait_read<kNbuf - 1>();
+// Shared-memory tile ring of nbuf tiles: `slot` counts tiles issued by this CTA; a tile buffer is
+// reused only after the bulk store that read it nbuf tiles ago has finished reading (thread 0
+// waits, the barrier publishes). Every tile commits exactly one bulk group.
+__device__ __forceinline__ void bulk_wait_read_n(int n) {
+  switch (n) {
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+    case 7: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+  }
+}
+__device__ __forceinline__ void stat_add(unsigned long long* st, int k, unsigned long long t0) {
+  if (st) atomicAdd(st + 4 * blockIdx.x + k, gtimer() - t0);
+}
+__device__ __forceinline__ float4* acquire_tile(float4* smem, int& slot, int nbuf, unsigned long long* st) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = st ? gtimer() : 0;
+    bulk_wait_read_n(nbuf - 1);
+    stat_add(st, 0, t0);
+  }
   __syncthreads();
-  float4* b = smem + (slot % kNbuf) * kTileF4;
+  float4* b = smem + (slot % nbuf) * kTileF4;
   ++slot;
   return b;
 }
 
 // A(o, c): my partial of chunk c of slice o -> owner o's staging row me (NVLink).
 template <int M, int U, bool MOM, bool BF>
-__device__ void stage_A(const XPart& p, int o, int64_t c, float4* smem, int& slot) {
+__device__ void stage_A(const XPart& p, int o, int64_t c, float4* smem, int& slot, int& ncommit, int nbuf,
+                        unsigned long long* st) {
   const ChunkRange r = chunk_range(p, o, c);
   const int64_t slo = slice_lo(p, o);
   float* dst = p.stage[o];
   for (int64_t t0 = r.lo; t0 < r.hi; t0 += kTileF4) {
-    float4* sb = acquire_tile(smem, slot);
+    float4* sb = acquire_tile(smem, slot, nbuf, st);
 #pragma unroll
     for (int r0 = 0; r0 < kTileRows; r0 += U) {
       float4 s[U];
@@ -329,6 +358,7 @@ __device__ void stage_A(const XPart& p, int o, int64_t c, float4* smem, int& slo
       const int64_t cnt = min(kTileF4, r.hi - t0);
       bulk_store(dst + stage_off(p, p.me, t0 - slo), sb, static_cast<uint32_t>(cnt * 16));  // NVLink
       bulk_commit();
+      ++ncommit;
     }
   }
   if (r.tail && threadIdx.x < p.rem) {
@@ -339,14 +369,15 @@ __device__ void stage_A(const XPart& p, int o, int64_t c, float4* smem, int& slo
 
 // B(c): fold my slice's chunk c over all GPUs, divide, store locally and push to every peer.
 template <int M, int U, bool MOM, bool BF, int KPM>
-__device__ void stage_B(const XPart& p, int64_t c, float4* smem, int& slot) {
+__device__ void stage_B(const XPart& p, int64_t c, float4* smem, int& slot, int& ncommit, int nbuf,
+                        unsigned long long* st) {
   const int o = p.me;
   const ChunkRange r = chunk_range(p, o, c);
   const int64_t slo = slice_lo(p, o);
   const float* stage = p.stage[o];  // my staging region (local)
   const float kf = static_cast<float>(p.k_total);
   for (int64_t t0 = r.lo; t0 < r.hi; t0 += kTileF4) {
-    float4* sb = acquire_tile(smem, slot);
+    float4* sb = acquire_tile(smem, slot, nbuf, st);
 #pragma unroll
     for (int r0 = 0; r0 < kTileRows; r0 += U) {
       const int64_t i0 = t0 + r0 * kRowF4 + threadIdx.x;
@@ -397,6 +428,7 @@ __device__ void stage_B(const XPart& p, int64_t c, float4* smem, int& slot) {
         if (bytes) bulk_store(dst, sb, bytes);  // NVLink
       }
       bulk_commit();
+      ++ncommit;
     }
   }
   if (r.tail && threadIdx.x < p.rem) {
@@ -453,16 +485,60 @@ __device__ __forceinline__ void prof_rec(const XTask& T, int pi, int kind, int64
   }
 }
 
+// cp.async.bulk.wait_group takes an immediate: wait until at most n (clamped to 63) of this
+// thread's most recent bulk groups are pending.
+__device__ __forceinline__ void bulk_wait_pending(int n) {
+  switch (n < 63 ? n : 63) {
+#define RP_W(k) \
+  case k: asm volatile("cp.async.bulk.wait_group " #k ";" ::: "memory"); break;
+#define RP_W8(k) RP_W(k) RP_W(k + 1) RP_W(k + 2) RP_W(k + 3) RP_W(k + 4) RP_W(k + 5) RP_W(k + 6) RP_W(k + 7)
+    RP_W8(0) RP_W8(8) RP_W8(16) RP_W8(24) RP_W8(32) RP_W8(40) RP_W8(48) RP_W8(56)
+#undef RP_W8
+#undef RP_W
+  }
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Publish the flags of the stores issued in an earlier iteration (thread 0): those bulk groups
+// have completed (caller waited), fence.proxy.async makes the async-proxy writes visible to the
+// generic proxy, one fence.acq_rel.sys + relaxed stores form the release (cumulative: the other
+// threads' plain tail stores are ordered by the barrier before it).
+__device__ __forceinline__ void post_flags(const XTask& T, const XPart& p, int64_t cA, int64_t cB) {
+  if (cA < 0 && cB < 0) return;
+  fence_async_all();
+  fence_acq_rel_sys();
+  if (cA >= 0)
+    for (int j = 1; j < p.kp; ++j) {
+      const int o = (p.me + j) % p.kp;
+      st_relaxed_sys(flag_at(p.pflags[o], p.slot, T.my_gpu, kFlagA, cA), p.tag[o]);
+    }
+  if (cB >= 0)
+    for (int d = 0; d < p.kp; ++d)
+      if (d != p.me) st_relaxed_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagB, cB), p.tag[d]);
+}
+
 // One lane of part pi: the pipelined iterations. false = a flag wait hit the watchdog.
+//
+// Iteration i issues A(c_i), B(c_{i-2}), C(c_{i-4}) and then publishes the flags of iteration
+// i-1's stores once those have completed, while iteration i's stores are still on the wire
+// (deferred signalling: a CTA never drains its NVLink pushes to post a flag; waiting for all of
+// them cost 10-25 % at 32-128 KB per flag, profiles/r02/bulk_push_probe_2gpu.txt). A(c) flags
+// are posted at the end of iteration c+1, so B(c) runs in iteration c+2 (the peers' flags are
+// one iteration old by then); B(c) flags at the end of c+3, so C(c) runs in c+4.
 template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
 __device__ bool run_lane(const XTask& T, int pi, int lane, float4* smem, int& slot, unsigned long long& ready_seen,
                          int* s_abort) {
   const XPart& p = T.part[pi];
   const int64_t iters = lane < p.nch ? (p.nch - 1 - lane) / kXLanes + 1 : 0;
-  for (int64_t i = 0; i < iters + 2; ++i) {
+  int64_t pA = -1, pB = -1;  // chunks whose stores the previous iteration issued (flags pending)
+  for (int64_t i = 0; i < (iters ? iters + 4 : 0); ++i) {
     const int64_t cA = i < iters ? lane + i * kXLanes : -1;
-    const int64_t cB = (i >= 1 && i - 1 < iters) ? lane + (i - 1) * kXLanes : -1;
-    const int64_t cC = (i >= 2 && i - 2 < iters) ? lane + (i - 2) * kXLanes : -1;
+    const int64_t cB = (i >= 2 && i - 2 < iters) ? lane + (i - 2) * kXLanes : -1;
+    const int64_t cC = (i >= 4 && i - 4 < iters) ? lane + (i - 4) * kXLanes : -1;
+    int ncommit = 0;  // bulk groups committed in this iteration (thread 0)
     unsigned long long ts = 0;
     if (cA >= 0) {
       if (T.prof && threadIdx.x == 0) ts = gtimer();
@@ -477,7 +553,7 @@ __device__ bool run_lane(const XTask& T, int pi, int lane, float4* smem, int& sl
         }
         __syncthreads();
         if (*s_abort) return false;
-        stage_A<M, UA, MOM, BF>(p, o, cA, smem, slot);
+        stage_A<M, UA, MOM, BF>(p, o, cA, smem, slot, ncommit, T.nbuf, T.cta_stat);
       }
       prof_rec(T, pi, 0, cA, ts, ts);
     }
@@ -494,7 +570,7 @@ __device__ bool run_lane(const XTask& T, int pi, int lane, float4* smem, int& sl
       __syncthreads();
       if (*s_abort) return false;
       if (T.prof && threadIdx.x == 0) tr = gtimer();
-      stage_B<M, UB, MOM, BF, KPM>(p, cB, smem, slot);
+      stage_B<M, UB, MOM, BF, KPM>(p, cB, smem, slot, ncommit, T.nbuf, T.cta_stat);
       prof_rec(T, pi, 1, cB, ts, tr);
     }
     if (cC >= 0) {
@@ -512,24 +588,19 @@ __device__ bool run_lane(const XTask& T, int pi, int lane, float4* smem, int& sl
         if (j == p.kp - 1) prof_rec(T, pi, 2, cC, ts, tr);
       }
     }
-    // signal: every bulk (and plain tail) store of this iteration has completed -> publish its
-    // flags. The release stores order the completed writes (the async proxy's made visible by
-    // fence.proxy.async; the other threads' tail stores by the barrier, release is cumulative);
-    // no separate fence.sc.sys: it cost 10-15 % of the push rate at 64-256 KB per flag
-    // (profiles/r02_bulk_push_probe_2gpu.txt)
     __syncthreads();
-    if (threadIdx.x == 0 && (cA >= 0 || cB >= 0)) {
-      bulk_wait_all();
-      fence_async_all();
-      if (cA >= 0)
-        for (int j = 1; j < p.kp; ++j) {
-          const int o = (p.me + j) % p.kp;
-          st_release_sys(flag_at(p.pflags[o], p.slot, T.my_gpu, kFlagA, cA), p.tag[o]);
-        }
-      if (cB >= 0)
-        for (int d = 0; d < p.kp; ++d)
-          if (d != p.me) st_release_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagB, cB), p.tag[d]);
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = T.cta_stat ? gtimer() : 0;
+      bulk_wait_pending(ncommit);  // the previous iteration's groups have completed
+      stat_add(T.cta_stat, 1, t0);
+      post_flags(T, p, pA, pB);
     }
+    pA = cA;
+    pB = cB;
+  }
+  if (threadIdx.x == 0 && (pA >= 0 || pB >= 0)) {  // (never: the last iterations issue only C)
+    bulk_wait_all();
+    post_flags(T, p, pA, pB);
   }
   return true;
 }
@@ -550,17 +621,21 @@ __device__ __forceinline__ void xgpu_body(const XTask& T, int cta, int ncta) {
     }
   }
   __syncthreads();
+  const unsigned long long t_begin = T.cta_stat ? gtimer() : 0;
   int slot = 0;
   unsigned long long ready_seen = 0;  // bit 8*pi + o: READY of part pi's owner o observed (thread 0)
   const int total = T.nparts * kXLanes;
   bool ok = true;
   for (int idx = cta; ok && idx < total; idx += ncta)
     ok = run_lane<M, UA, UB, MOM, BF, KPM>(T, idx % T.nparts, idx / T.nparts, xsmem, slot, ready_seen, &s_abort);
-  if (threadIdx.x == 0) bulk_wait_all();  // never leave with a bulk store reading shared memory
+  if (threadIdx.x == 0) {
+    bulk_wait_all();  // never leave with a bulk store reading shared memory
+    stat_add(T.cta_stat, 3, t_begin);
+  }
 }
 
 template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
-__global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const __grid_constant__ XTask T) {
+__global__ void __launch_bounds__(kXThreads, RP_XGPU_MINB) xgpu_kernel(const __grid_constant__ XTask T) {
   xgpu_body<M, UA, UB, MOM, BF, KPM>(T, blockIdx.x, gridDim.x);
 }
 
@@ -568,18 +643,24 @@ __global__ void __launch_bounds__(kXThreads, 2) xgpu_kernel(const __grid_constan
 // virtual GPU v on CTAs v, v + V, v + 2V, ... (all co-resident: a spinning CTA never starves the
 // CTA it waits for; separate spinning launches on one GPU are not guaranteed to run together).
 template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
-__global__ void __launch_bounds__(kXThreads, 2) xgpu_emul_kernel(const XTask* __restrict__ tasks, int V) {
+__global__ void __launch_bounds__(kXThreads, RP_XGPU_MINB) xgpu_emul_kernel(const XTask* __restrict__ tasks, int V) {
   const int v = blockIdx.x % V;
   xgpu_body<M, UA, UB, MOM, BF, KPM>(tasks[v], blockIdx.x / V, gridDim.x / V);
 }
 
 int g_sms = 0;
-constexpr size_t kSmem = static_cast<size_t>(kNbuf) * kTileF4 * sizeof(float4);
-
 int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : def;
 }
+
+constexpr size_t kSmemMax = static_cast<size_t>(kNbufMax) * kTileF4 * sizeof(float4);
+int nbuf_setting() {
+  static const int v = std::min(kNbufMax, std::max(2, env_int("RP_XGPU_NBUF", kNbufDefault)));
+  return v;
+}
+size_t smem_bytes(int nbuf) { return static_cast<size_t>(nbuf) * kTileF4 * sizeof(float4); }
+
 
 int sm_count() {
   if (g_sms == 0) {
@@ -594,7 +675,7 @@ int sm_count() {
 // 48 KB of dynamic shared memory + the static words exceed the default 48 KB per-CTA limit
 template <typename F>
 bool smem_attr(F fn) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)) ==
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemMax)) ==
          cudaSuccess;
 }
 
@@ -606,7 +687,8 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
       *err = "xgpu: shared memory attribute";
       return RP_ECUDA;
     }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, UA, UB, MOM, BF, KPM>, kXThreads, kSmem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_kernel<M, UA, UB, MOM, BF, KPM>, kXThreads,
+                                                      smem_bytes(nbuf_setting())) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
@@ -617,7 +699,8 @@ int launch_m(XTask& T, cudaStream_t stream, std::string* err) {
   if (cps > 0) grid = std::min<int64_t>(grid, static_cast<int64_t>(sm_count()) * cps);
   if (T.max_ctas > 0) grid = std::min<int64_t>(grid, T.max_ctas);
   grid = std::max<int64_t>(1, std::min<int64_t>(grid, static_cast<int64_t>(T.nparts) * kXLanes));
-  xgpu_kernel<M, UA, UB, MOM, BF, KPM><<<static_cast<int>(grid), kXThreads, kSmem, stream>>>(T);
+  T.nbuf = nbuf_setting();
+  xgpu_kernel<M, UA, UB, MOM, BF, KPM><<<static_cast<int>(grid), kXThreads, smem_bytes(T.nbuf), stream>>>(T);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("xgpu kernel launch: ") + cudaGetErrorString(e);
@@ -638,7 +721,8 @@ int launch_emul_m(const XTask* d_tasks, int V, int max_parts, cudaStream_t strea
     attr = true;
   }
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kXThreads, kSmem) != cudaSuccess || occ < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kXThreads, smem_bytes(nbuf_setting())) != cudaSuccess ||
+      occ < 1) {
     *err = "xgpu emulation: occupancy query failed";
     return RP_ECUDA;
   }
@@ -651,7 +735,7 @@ int launch_emul_m(const XTask* d_tasks, int V, int max_parts, cudaStream_t strea
   int grid = static_cast<int>(per * V);
   void* args[] = {const_cast<XTask**>(&d_tasks), &V};
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kXThreads),
-                                                    args, kSmem, stream);
+                                                    args, smem_bytes(nbuf_setting()), stream);
   if (e != cudaSuccess) {
     *err = std::string("xgpu emulation cooperative launch: ") + cudaGetErrorString(e);
     return RP_ECUDA;
@@ -687,8 +771,8 @@ int dispatch(XTask& T, const XTask* d_tasks, int V, int max_parts, cudaStream_t 
     RP_XL(8, 1, 1, true, false, 8);
   }
   if (kpmax <= 2 && !EMU) {
-    if (mmax <= 1) RP_XL(1, 4, 2, false, false, 2);
-    if (mmax <= 2) RP_XL(2, 2, 1, false, false, 2);
+    if (mmax <= 1) RP_XL(1, 4, 4, false, false, 2);
+    if (mmax <= 2) RP_XL(2, 2, 2, false, false, 2);
     if (mmax <= 4) RP_XL(4, 1, 1, false, false, 2);
     RP_XL(8, 1, 1, false, false, 2);
   }
@@ -736,15 +820,31 @@ int check_task(const XTask& T, int* mmax, int* kpmax, bool* mom, std::string* er
 
 }  // namespace
 
+// RP_XGPU_V2=1: the register (LDG/STG) version of this file for plain SGD too (comparison);
+// momentum steps always take it (their buffers are read and written per member)
+int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stages (tuning)
+  static const int v = std::max(2, std::min(6, env_int("RP_XGPU_BLAG", 2)));
+  return v;
+}
+
+bool use_v2() {
+  static const int v = env_int("RP_XGPU_V2", 0);
+  return v == 1;
+}
+
 void xgpu_geometry(XPart& p, int64_t n) {
   p.n4 = n / 4;
   p.rem = static_cast<int32_t>(n - 4 * p.n4);
   p.S4 = ((p.n4 + p.kp - 1) / p.kp + kTileF4 - 1) / kTileF4 * kTileF4;
   p.S4 = std::max<int64_t>(p.S4, kTileF4);
-  // about kLaneIters pipeline iterations per lane, whole tiles, at most kMaxChunks chunks
-  const int64_t ch = std::max<int64_t>((p.S4 + kXLanes * kLaneIters - 1) / (kXLanes * kLaneIters),
+  // about kLaneIters pipeline iterations per lane, whole tiles of at least kMinTiles, at most
+  // kMaxChunks chunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job
+  // must see the same values: the geometry must agree across GPUs)
+  static const int iters = std::max(1, env_int("RP_XGPU_ITERS", kLaneIters));
+  static const int min_tiles = std::max(1, env_int("RP_XGPU_MIN_TILES", kMinTiles));
+  const int64_t ch = std::max<int64_t>((p.S4 + kXLanes * iters - 1) / (kXLanes * iters),
                                        (p.S4 + kMaxChunks - 1) / kMaxChunks);
-  p.CH = std::max<int64_t>(kTileF4, (ch + kTileF4 - 1) / kTileF4 * kTileF4);
+  p.CH = std::max<int64_t>(kTileF4 * min_tiles, (ch + kTileF4 - 1) / kTileF4 * kTileF4);
   p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
 }
 
@@ -758,6 +858,8 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   bool mom = false;
   const int rc = check_task(T, &mmax, &kpmax, &mom, err);
   if (rc != RP_OK) return rc;
+  T.blag = blag_setting();
+  if (!mom && !use_v2()) return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
   return dispatch<false>(T, nullptr, 1, T.nparts, static_cast<cudaStream_t>(stream), err, mmax, kpmax, mom);
 }
 
@@ -771,11 +873,16 @@ int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std:
     max_parts = std::max(max_parts, static_cast<int>(tasks[v].nparts));
   }
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int v = 0; v < V; ++v) {
+    tasks[v].nbuf = nbuf_setting();
+    tasks[v].blag = blag_setting();
+  }
   const cudaError_t e = cudaMemcpyAsync(d_tasks, tasks, sizeof(XTask) * V, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) {
     *err = std::string("xgpu emulation: task upload: ") + cudaGetErrorString(e);
     return RP_ECUDA;
   }
+  if (!mom && !use_v2()) return launch_xgpu_ws(tasks[0], d_tasks, V, max_parts, stream, err, mmax, kpmax, true);
   // generic instantiations (KPM 8): emulation is a parity tool, not a timed path
   return dispatch<true>(tasks[0], d_tasks, V, max_parts, s, err, mmax, 8, mom);
 }

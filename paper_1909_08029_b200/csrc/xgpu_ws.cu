@@ -1,0 +1,703 @@
+// Cross-GPU fused SGD + P-Reduce, warp-specialized (default for plain-SGD steps, fp32 and bf16).
+//
+// Same method, geometry, work order and flag protocol as xgpu.cu (read its header first): a
+// group on GPUs d_0 < ... < d_{kp-1} is a reduce-scatter + all-gather fused with alg1 step 2
+// and the pre-reduction of co-resident members (reading R1); chunk c runs on lane
+// c mod kXLanes; a lane is the pipeline {A(c_i), B(c_{i-2}), C(c_{i-4}), signal(i-1)}.
+//
+// What changes is how a CTA moves the bytes. Round 2 measured the LDG/STG version per CTA
+// (RP_XGPU_PROFILE breakdown, profiles/r02/): 65-96 % of a CTA's time went to loading x, g and
+// the staged partials and folding them, < 2 % to waiting for its NVLink pushes -- the pushes
+// were starved by the loads. Here one producer warp streams every operand tile of the lane's
+// work into an S-stage shared-memory ring with TMA bulk loads (cp.async.bulk global ->
+// shared, completion on the stage's `full` mbarrier), waiting for the peers' flags before a
+// stage that needs their data; eight consumer warps fold each stage into an output tile and
+// push it with TMA bulk stores (to the owner's staging for A, to the local members and every
+// peer's first member for B, to the other local members for C), then release the stage on its
+// `empty` mbarrier. Loads, arithmetic and NVLink pushes of different tiles overlap.
+//
+// Flags (deferred, as in xgpu.cu): a SIG job ends every lane iteration; each consumer warp
+// waits until only its bulk groups of this iteration are pending (so its groups of the
+// previous iteration have completed), makes them visible to the generic proxy and arrives on a
+// shared counter with acq_rel; the last warp releases at system scope and posts the previous
+// iteration's A and B flags. A wait for a peer's flag (producer warp) past the watchdog limit
+// records it in host-mapped memory and ends the CTA's work (an END job lets the consumers out).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "rp_internal.h"
+#include "update.cuh"
+
+namespace rp {
+namespace {
+
+constexpr int kWarps = 8;                       // consumer warps
+constexpr int kWsT = 32 * (kWarps + 1);         // + one producer warp
+constexpr int kT = 512;                         // vectors per tile (8 KB per fp32 operand)
+constexpr int kPW = kT / kWarps;                // vectors per consumer warp and tile
+constexpr int kVPL = kPW / 32;                  // vectors per lane and tile
+constexpr int kGeomTile = 1024;                 // xgpu.cu's chunk / slice alignment (vectors)
+constexpr int kSigRing = 8;                     // SIG counters (> max stages)
+constexpr int kJA = 0, kJB = 1, kJC = 2, kJSig = 3, kJEnd = 4;
+
+struct Job {                // one stage's work, written by the producer next to the stage
+  int32_t kind, pi, o, cnt;
+  int64_t base;             // first vector of the tile (absolute index in the replica)
+  int64_t pA, pB;           // SIG: chunks whose flags to post
+  int32_t tail;             // the chunk's n mod 4 scalar tail rides on this job
+  int32_t sig;              // SIG sequence number
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_pending(int n) {
+  switch (n < 63 ? n : 63) {
+#define RP_W(k) \
+  case k: asm volatile("cp.async.bulk.wait_group " #k ";" ::: "memory"); break;
+#define RP_W8(k) RP_W(k) RP_W(k + 1) RP_W(k + 2) RP_W(k + 3) RP_W(k + 4) RP_W(k + 5) RP_W(k + 6) RP_W(k + 7)
+    RP_W8(0) RP_W8(8) RP_W8(16) RP_W8(24) RP_W8(32) RP_W8(40) RP_W8(48) RP_W8(56)
+#undef RP_W8
+#undef RP_W
+  }
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int atom_add_acq_rel_cta(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 div4(float4 a, float k) {
+  return make_float4(__fdiv_rn(a.x, k), __fdiv_rn(a.y, k), __fdiv_rn(a.z, k), __fdiv_rn(a.w, k));
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t bf_rn(float v) {  // IEEE round-to-nearest-even; NaN stays NaN
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
+}
+__device__ __forceinline__ uint2 pack_bf4(float4 v) {
+  return make_uint2(bf_rn(v.x) | (bf_rn(v.y) << 16), bf_rn(v.z) | (bf_rn(v.w) << 16));
+}
+__device__ __forceinline__ float4 unpack_bf4(uint2 w) { return make_float4(bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y)); }
+
+// flag word of (slot, src GPU, kind, chunk) in a GPU's flag array (layout of xgpu.cu)
+__device__ __forceinline__ unsigned long long* flag_at(unsigned long long* base, int slot, int src, int kind,
+                                                       int64_t c) {
+  return base + (static_cast<int64_t>(slot) * kFlagSrc + src) * kFlagStride +
+         (kind == kFlagA ? c : (kind == kFlagB ? kMaxChunks + c : 2 * kMaxChunks));
+}
+
+__device__ __noinline__ bool wait_flag_slow(const XTask& T, const unsigned long long* f, unsigned long long tag,
+                                            int slot, int src, int kind, int64_t c) {
+  const unsigned long long t0 = gtimer();
+  for (unsigned n = 1;; ++n) {
+    __nanosleep(32);
+    if (ld_acquire_sys(f) == tag) return true;
+    if (T.watchdog_ns && (n & 1023u) == 0) {
+      if (T.err && *reinterpret_cast<volatile unsigned long long*>(&T.err->code)) return false;  // job failed
+      if (gtimer() - t0 <= T.watchdog_ns) continue;
+      if (T.err && atomicCAS(&T.err->code, 0ull, 1ull) == 0ull) {
+        T.err->gpu = T.my_gpu;
+        T.err->src = src;
+        T.err->kind = kind;
+        T.err->slot = slot;
+        T.err->chunk = c;
+        T.err->tag = tag;
+        T.err->seen = ld_acquire_sys(f);
+        __threadfence_system();
+      }
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ bool wait_flag(const XTask& T, const unsigned long long* f, unsigned long long tag,
+                                          int slot, int src, int kind, int64_t c) {
+  if (ld_acquire_sys(f) == tag) return true;
+  const unsigned long long t0 = T.cta_stat ? gtimer() : 0;
+  const bool ok = wait_flag_slow(T, f, tag, slot, src, kind, c);
+  if (T.cta_stat) atomicAdd(T.cta_stat + 4 * blockIdx.x + 2, gtimer() - t0);
+  return ok;
+}
+
+struct Range {
+  int64_t lo, hi;
+  bool tail;
+};
+__device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(static_cast<int64_t>(o) * p.S4, p.n4); }
+__device__ __forceinline__ Range chunk_range(const XPart& p, int o, int64_t c) {
+  const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
+  Range r;
+  r.lo = min(slo + c * p.CH, shi);
+  r.hi = min(slo + (c + 1) * p.CH, shi);
+  r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
+  return r;
+}
+__device__ __forceinline__ int64_t stage_off(const XPart& p, int d, int64_t i_rel) {
+  return (static_cast<int64_t>(d) * (p.S4 + 1) + i_rel) * 4;
+}
+
+// ---- scalar tails (n mod 4 elements; plain global loads / stores, warp 0 of the consumers) ----
+template <bool BF>
+__device__ __forceinline__ float ldx1(const float* base, int64_t j) {
+  if constexpr (BF) return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(base)[j]) << 16);
+  else return base[j];
+}
+template <bool BF>
+__device__ __forceinline__ void stx1(float* base, int64_t j, float v) {
+  if constexpr (BF) reinterpret_cast<uint16_t*>(base)[j] = static_cast<uint16_t>(bf_rn(v));
+  else base[j] = v;
+}
+template <int M, bool BF>
+__device__ __forceinline__ float partial1(const XPart& p, int64_t j) {
+  float s = 0.f;
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+    if (m < p.m) {
+      float y = ldx1<BF>(p.x[m], j);
+      if (p.u[m].g) y = step_sgd(y, ldx1<BF>(p.u[m].g, j), p.u[m].lr);
+      s = m == 0 ? y : __fadd_rn(s, y);
+    }
+  return s;
+}
+
+// Shared-memory layout: S stages of NOP operand slots of kT vectors (16 bytes per vector per slot,
+// bf16 operands use the first half), the output tiles [2][kT], S full + S empty mbarriers,
+// S job descriptors, the SIG counters and the abort word.
+template <int NOP, int S>
+constexpr size_t ws_smem() {
+  return static_cast<size_t>(S) * NOP * kT * 16 + 2 * kT * 16 + 2 * S * 8 + S * sizeof(Job) + kSigRing * 4 + 16;
+}
+
+// ---- consumer side ----
+template <int M, int KPM, bool BF>
+__device__ __forceinline__ void consume(const XTask& T, const Job& J, const float4* st, float4* out, int ob, int warp,
+                                        int lane, int& ncommit) {
+  const XPart& p = T.part[J.pi];
+  const int e0 = warp * kPW;
+  const int mine = max(0, min(kPW, J.cnt - e0));
+  // operand slot q, vector e: fp32 16 B; bf16 8 B (first half of the slot)
+  auto opf = [&](int q, int e) { return st[q * kT + e]; };
+  auto opb = [&](int q, int e) { return unpack_bf4(reinterpret_cast<const uint2*>(st + q * kT)[e]); };
+  if (J.kind == kJC) {
+    // xbar of this tile (slot 0, already rounded for bf16) -> the other local members
+#pragma unroll
+    for (int j = 0; j < kVPL; ++j) {
+      const int e = e0 + j * 32 + lane;
+      if (e < J.cnt) {
+        if constexpr (BF) reinterpret_cast<uint2*>(out + ob * kT)[e] = reinterpret_cast<const uint2*>(st)[e];
+        else out[ob * kT + e] = st[e];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kVPL; ++j) {
+      const int e = e0 + j * 32 + lane;
+      if (e >= J.cnt) continue;
+      const int64_t i = J.base + e;
+      // bf16: an odd last vector of the replica was not bulk-loaded (16-byte granules)
+      const bool odd_last = BF && (J.cnt & 1) && e == J.cnt - 1;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if (m >= p.m) break;
+        float4 x, g;
+        if constexpr (BF) {
+          if (odd_last) {
+            const uint2 xw = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.x[m]) + 4 * i);
+            x = unpack_bf4(xw);
+            if (p.u[m].g) g = unpack_bf4(*reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.u[m].g) + 4 * i));
+          } else {
+            x = opb(2 * m, e);
+            if (p.u[m].g) g = opb(2 * m + 1, e);
+          }
+        } else {
+          x = opf(2 * m, e);
+          if (p.u[m].g) g = opf(2 * m + 1, e);
+        }
+        float4 vdummy;
+        const float4 y = step4<false>(x, g, vdummy, p.u[m]);
+        s = m == 0 ? y : add4(s, y);
+      }
+      if (J.kind == kJA) {
+        out[ob * kT + e] = s;  // fp32 partial
+      } else {  // B: fold the partials in ascending GPU id, divide (reading R1)
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int q = 2 * M;
+#pragma unroll
+        for (int d = 0; d < KPM; ++d) {
+          if (d >= p.kp) break;
+          const float4 v = d == p.me ? s : opf(q++, e);
+          acc = d == 0 ? v : add4(acc, v);
+        }
+        const float4 xbar = div4(acc, static_cast<float>(p.k_total));
+        if constexpr (BF) {
+          reinterpret_cast<uint2*>(out + ob * kT)[e] = pack_bf4(xbar);
+          if (odd_last) {  // plain stores of the odd last vector (bulk copies move 16-byte granules)
+            const uint2 w = pack_bf4(xbar);
+            for (int m = 0; m < p.m; ++m) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.x[m]) + 4 * i) = w;
+            for (int d = 0; d < p.kp; ++d)
+              if (d != p.me) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.xfirst[d]) + 4 * i) = w;  // NVLink
+          }
+        } else {
+          out[ob * kT + e] = xbar;
+        }
+      }
+    }
+  }
+  if (J.kind == kJC && BF && (J.cnt & 1) && lane == 0 && e0 <= J.cnt - 1 && J.cnt - 1 < e0 + kPW) {
+    const int64_t i = J.base + J.cnt - 1;  // odd last bf16 vector: not bulk-loaded, copy it directly
+    const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.x[0]) + 4 * i);
+    for (int m = 1; m < p.m; ++m) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.x[m]) + 4 * i) = w;
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0 && mine > 0) {
+    const float4* src = out + ob * kT + e0;
+    const char* srcb = reinterpret_cast<const char*>(BF ? static_cast<const void*>(reinterpret_cast<const uint2*>(out + ob * kT) + e0)
+                                                       : static_cast<const void*>(src));
+    if (J.kind == kJA) {
+      const int64_t slo = slice_lo(p, J.o);
+      bulk_store(p.stage[J.o] + stage_off(p, p.me, J.base + e0 - slo), src, static_cast<uint32_t>(mine * 16));  // NVLink
+    } else {
+      int nb = mine;
+      if (BF && (J.cnt & 1) && e0 + mine == J.cnt) nb = mine - 1;  // the odd last vector went by plain stores
+      const uint32_t bytes = static_cast<uint32_t>(nb * (BF ? 8 : 16));
+      const int64_t off = BF ? 8 * (J.base + e0) : 16 * (J.base + e0);
+      if (bytes) {
+        if (J.kind == kJB) {
+          for (int m = 0; m < p.m; ++m) bulk_store(reinterpret_cast<char*>(p.x[m]) + off, srcb, bytes);
+          for (int jj = 1; jj < p.kp; ++jj) {
+            const int d = (p.me + jj) % p.kp;  // spread the pushes over the peers
+            bulk_store(reinterpret_cast<char*>(p.xfirst[d]) + off, srcb, bytes);  // NVLink
+          }
+        } else {  // C
+          for (int m = 1; m < p.m; ++m) bulk_store(reinterpret_cast<char*>(p.x[m]) + off, srcb, bytes);
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    bulk_commit();
+    ++ncommit;
+  }
+}
+
+// scalar tail of a chunk (warp 0's lanes < rem), after the chunk's last tile job
+template <int M, int KPM, bool BF>
+__device__ __forceinline__ void tail_job(const XPart& p, int kind, int o, int lane) {
+  if (lane >= p.rem) return;
+  const int64_t j = 4 * p.n4 + lane;
+  if (kind == kJA) {
+    const int64_t slo = slice_lo(p, o);
+    p.stage[o][stage_off(p, p.me, p.n4 - slo) + lane] = partial1<M, BF>(p, j);  // NVLink (plain store)
+  } else if (kind == kJB) {
+    const int64_t so = p.n4 - slice_lo(p, p.me);
+    const float* stg = p.stage[p.me];
+    const float mine = partial1<M, BF>(p, j);
+    float s = p.me == 0 ? mine : stg[stage_off(p, 0, so) + lane];
+    for (int d = 1; d < p.kp; ++d) s = __fadd_rn(s, d == p.me ? mine : stg[stage_off(p, d, so) + lane]);
+    const float xbar = __fdiv_rn(s, static_cast<float>(p.k_total));
+    for (int m = 0; m < p.m; ++m) stx1<BF>(p.x[m], j, xbar);
+    for (int d = 0; d < p.kp; ++d)
+      if (d != p.me) stx1<BF>(p.xfirst[d], j, xbar);  // NVLink
+  } else {
+    const float v = ldx1<BF>(p.x[0], j);
+    for (int m = 1; m < p.m; ++m) stx1<BF>(p.x[m], j, v);
+  }
+}
+
+// ---- producer side ----
+struct Prod {
+  int s = 0, it = 0;
+  uint32_t phase = 0;
+};
+
+template <int NOP, int S>
+__device__ __forceinline__ int acquire_stage(Prod& P, uint64_t* empty) {
+  if (P.it >= S) mbar_wait(&empty[P.s], P.phase ^ 1u);
+  return P.s;
+}
+template <int S>
+__device__ __forceinline__ void advance(Prod& P) {
+  ++P.it;
+  if (++P.s == S) {
+    P.s = 0;
+    P.phase ^= 1u;
+  }
+}
+
+template <int M, int KPM, bool BF, int NOP, int S>
+__device__ void produce_tiles(const XTask& T, int pi, int kind, int o, int64_t c, float4* stages, uint64_t* full,
+                              uint64_t* empty, Job* jobs, Prod& P) {
+  const XPart& p = T.part[pi];
+  const Range r = chunk_range(p, kind == kJB ? p.me : o, c);
+  const bool need_tail = r.tail && (kind != kJC || p.m > 1);
+  for (int64_t t0 = r.lo; t0 < r.hi || (t0 == r.lo && need_tail); t0 += kT) {
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kT), r.hi - t0));
+    const int s = acquire_stage<NOP, S>(P, empty);
+    Job& J = jobs[s];
+    J.kind = kind;
+    J.pi = pi;
+    J.o = o;
+    J.cnt = cnt;
+    J.base = t0;
+    J.tail = need_tail && t0 + kT >= r.hi;
+    float4* st = stages + static_cast<size_t>(s) * NOP * kT;
+    // bf16 operands: whole 16-byte granules only (an odd last vector is read directly)
+    const uint32_t xb = static_cast<uint32_t>(BF ? (cnt & ~1) * 8 : cnt * 16);
+    const uint32_t pb = static_cast<uint32_t>(cnt * 16);
+    uint32_t tot = 0;
+    if (kind == kJC) {
+      tot = xb;
+    } else {
+      for (int m = 0; m < p.m; ++m) tot += p.u[m].g ? 2 * xb : xb;
+      if (kind == kJB) tot += (p.kp - 1) * pb;
+    }
+    if (tot == 0) {
+      mbar_arrive(&full[s]);
+    } else {
+      mbar_expect_tx(&full[s], tot);
+      const int64_t eo = BF ? 8 * t0 : 16 * t0;  // byte offset of the tile in a replica
+      if (kind == kJC) {
+        if (xb) bulk_load(st, reinterpret_cast<const char*>(p.x[0]) + eo, xb, &full[s]);
+      } else {
+        for (int m = 0; m < p.m; ++m) {
+          if (xb) bulk_load(st + (2 * m) * kT, reinterpret_cast<const char*>(p.x[m]) + eo, xb, &full[s]);
+          if (p.u[m].g && xb) bulk_load(st + (2 * m + 1) * kT, reinterpret_cast<const char*>(p.u[m].g) + eo, xb, &full[s]);
+        }
+        if (kind == kJB) {
+          const int64_t slo = slice_lo(p, p.me);
+          int q = 2 * M;
+          for (int d = 0; d < p.kp; ++d)
+            if (d != p.me) bulk_load(st + (q++) * kT, p.stage[p.me] + stage_off(p, d, t0 - slo), pb, &full[s]);
+        }
+      }
+    }
+    advance<S>(P);
+    if (r.hi <= r.lo) break;  // tail-only job
+  }
+}
+
+template <int NOP, int S>
+__device__ __forceinline__ void produce_marker(int kind, int pi, int64_t pA, int64_t pB, int sig, uint64_t* full,
+                                               uint64_t* empty, Job* jobs, Prod& P) {
+  const int s = acquire_stage<NOP, S>(P, empty);
+  Job& J = jobs[s];
+  J.kind = kind;
+  J.pi = pi;
+  J.cnt = 0;
+  J.pA = pA;
+  J.pB = pB;
+  J.sig = sig;
+  J.tail = 0;
+  mbar_arrive(&full[s]);
+  advance<S>(P);
+}
+
+template <int M, int KPM, bool BF, int NOP, int S>
+__device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) {
+  extern __shared__ __align__(128) float4 wsmem[];
+  float4* stages = wsmem;
+  float4* out = stages + static_cast<size_t>(S) * NOP * kT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(out + 2 * kT);
+  uint64_t* empty = full + S;
+  Job* jobs = reinterpret_cast<Job*>(empty + S);
+  int* sigcnt = reinterpret_cast<int*>(jobs + S);
+  int* abort_w = sigcnt + kSigRing;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    for (int q = 0; q < kSigRing; ++q) sigcnt[q] = 0;
+    *abort_w = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int total = T.nparts * kXLanes;
+  if (warp == kWarps) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      if (cta == 0)  // READY: my staging is free for these groups (my previous kernel has finished)
+        for (int pi = 0; pi < T.nparts; ++pi) {
+          const XPart& p = T.part[pi];
+          for (int d = 0; d < p.kp; ++d)
+            if (d != p.me) st_release_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagReady, 0), p.tag[d]);
+        }
+      Prod P;
+      unsigned long long ready_seen = 0;
+      int sig = 0;
+      bool ok = true;
+      for (int idx = cta; ok && idx < total; idx += ncta) {
+        const int pi = idx % T.nparts, ln = idx / T.nparts;
+        const XPart& p = T.part[pi];
+        const int64_t iters = ln < p.nch ? (p.nch - 1 - ln) / kXLanes + 1 : 0;
+        int64_t pA = -1, pB = -1;
+        // B runs bl >= 2 iterations after A (A(c) flags are posted at the end of iteration c+1),
+        // C runs 2 bl after A (B(c) flags at the end of iteration c+bl+1)
+        const int bl = T.blag, cl = 2 * T.blag;
+        for (int64_t i = 0; ok && i < (iters ? iters + cl : 0); ++i) {
+          const int64_t cA = i < iters ? ln + i * kXLanes : -1;
+          const int64_t cB = (i >= bl && i - bl < iters) ? ln + (i - bl) * kXLanes : -1;
+          const int64_t cC = (i >= cl && i - cl < iters) ? ln + (i - cl) * kXLanes : -1;
+          if (cA >= 0)
+            for (int j = 1; ok && j < p.kp; ++j) {
+              const int o = (p.me + j) % p.kp;  // spread the pushes over the owners
+              const unsigned long long bit = 1ull << (8 * pi + o);
+              if (!(ready_seen & bit)) {
+                ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[o], kFlagReady, 0), p.tag[o], p.slot, p.gpu[o],
+                               kFlagReady, 0);
+                ready_seen |= bit;
+              }
+              if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJA, o, cA, stages, full, empty, jobs, P);
+            }
+          if (ok && cB >= 0) {
+            for (int d = 0; ok && d < p.kp; ++d)
+              if (d != p.me)
+                ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, cB), p.tag[d], p.slot, p.gpu[d],
+                               kFlagA, cB);
+            fence_async_all();  // the peers' partials (acquired) are read next by the async proxy
+            if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJB, p.me, cB, stages, full, empty, jobs, P);
+          }
+          if (ok && cC >= 0)
+            for (int j = 1; ok && j < p.kp; ++j) {
+              const int o = (p.me + j) % p.kp;
+              ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[o], kFlagB, cC), p.tag[o], p.slot, p.gpu[o],
+                             kFlagB, cC);
+              fence_async_all();
+              if (ok && p.m > 1) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJC, o, cC, stages, full, empty, jobs, P);
+            }
+          if (ok) produce_marker<NOP, S>(kJSig, pi, pA, pB, sig++, full, empty, jobs, P);
+          pA = cA;
+          pB = cB;
+        }
+      }
+      if (!ok) *reinterpret_cast<volatile int*>(abort_w) = 1;
+      produce_marker<NOP, S>(kJEnd, 0, -1, -1, 0, full, empty, jobs, P);
+    }
+    __syncwarp();
+  } else {  // ---------------- consumers ----------------
+    int ncommit = 0, ntile = 0;
+    const unsigned long long t_begin = T.cta_stat && lane == 0 && warp == 0 ? gtimer() : 0;
+    for (int it = 0;; ++it) {
+      const int s = it % S;
+      unsigned long long tw = 0;
+      if (T.cta_stat && warp == 0 && lane == 0) tw = gtimer();
+      mbar_wait(&full[s], static_cast<uint32_t>((it / S) & 1));
+      if (T.cta_stat && warp == 0 && lane == 0) atomicAdd(T.cta_stat + 4 * blockIdx.x + 0, gtimer() - tw);
+      const Job J = jobs[s];
+      if (J.kind == kJEnd) break;
+      if (J.kind == kJSig) {
+        if (lane == 0) {
+          mbar_arrive(&empty[s]);
+          unsigned long long t1 = T.cta_stat && warp == 0 ? gtimer() : 0;
+          bulk_wait_pending(ncommit);  // this warp's groups of the previous iteration have completed
+          if (T.cta_stat && warp == 0) atomicAdd(T.cta_stat + 4 * blockIdx.x + 1, gtimer() - t1);
+          ncommit = 0;
+          fence_async_all();
+          int* cnt = &sigcnt[J.sig % kSigRing];
+          if (atom_add_acq_rel_cta(cnt, 1) == kWarps - 1) {  // the last warp posts the flags
+            *cnt = 0;
+            const XPart& p = T.part[J.pi];
+            if (J.pA >= 0 || J.pB >= 0) {
+              asm volatile("fence.acq_rel.sys;" ::: "memory");
+              if (J.pA >= 0)
+                for (int j = 1; j < p.kp; ++j) {
+                  const int o = (p.me + j) % p.kp;
+                  st_relaxed_sys(flag_at(p.pflags[o], p.slot, T.my_gpu, kFlagA, J.pA), p.tag[o]);
+                }
+              if (J.pB >= 0)
+                for (int d = 0; d < p.kp; ++d)
+                  if (d != p.me) st_relaxed_sys(flag_at(p.pflags[d], p.slot, T.my_gpu, kFlagB, J.pB), p.tag[d]);
+            }
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      const float4* st = stages + static_cast<size_t>(s) * NOP * kT;
+      // every consumed tile commits one bulk group per warp and alternates the output buffer:
+      // the group that read out[ntile & 1] two tiles ago must have finished reading it
+      if (lane == 0) bulk_wait_read1();
+      __syncwarp();
+      consume<M, KPM, BF>(T, J, st, out, ntile & 1, warp, lane, ncommit);
+      ++ntile;
+      // the scalar tail rides on the chunk's last job (warp 0); the other warps release the stage
+      if (J.tail && warp == 0) {
+        const XPart& p = T.part[J.pi];
+        if (J.kind == kJA) tail_job<M, KPM, BF>(p, kJA, J.o, lane);
+        else if (J.kind == kJB) tail_job<M, KPM, BF>(p, kJB, 0, lane);
+        else tail_job<M, KPM, BF>(p, kJC, J.o, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (lane == 0) bulk_wait_all();
+    if (T.cta_stat && warp == 0 && lane == 0) atomicAdd(T.cta_stat + 4 * blockIdx.x + 3, gtimer() - t_begin);
+  }
+}
+
+template <int M, int KPM, bool BF, int NOP, int S, int MINB>
+__global__ void __launch_bounds__(kWsT, MINB) xgpu_ws_kernel(const __grid_constant__ XTask T) {
+  xgpu_ws_body<M, KPM, BF, NOP, S>(T, blockIdx.x, gridDim.x);
+}
+template <int M, int KPM, bool BF, int NOP, int S, int MINB>
+__global__ void __launch_bounds__(kWsT, MINB) xgpu_ws_emul_kernel(const XTask* __restrict__ tasks, int V) {
+  const int v = blockIdx.x % V;
+  xgpu_ws_body<M, KPM, BF, NOP, S>(tasks[v], blockIdx.x / V, gridDim.x / V);
+}
+
+int g_ws_sms = 0;
+int ws_sms() {
+  if (g_ws_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_ws_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_ws_sms <= 0) g_ws_sms = 148;
+  }
+  return g_ws_sms;
+}
+
+template <int M, int KPM, bool BF, int NOP, int S, int MINB>
+int launch_ws_m(XTask& T, const XTask* d_tasks, int V, int max_parts, cudaStream_t stream, std::string* err, bool emu) {
+  constexpr size_t smem = ws_smem<NOP, S>();
+  static_assert(smem <= 227 * 1024, "shared memory");
+  static bool attr = false;
+  static int occ = 0, occ_emu = 0;
+  if (!attr) {
+    if (cudaFuncSetAttribute(xgpu_ws_kernel<M, KPM, BF, NOP, S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(xgpu_ws_emul_kernel<M, KPM, BF, NOP, S, MINB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+      *err = "xgpu_ws: shared memory attribute";
+      return RP_ECUDA;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xgpu_ws_kernel<M, KPM, BF, NOP, S, MINB>, kWsT, smem) !=
+            cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_emu, xgpu_ws_emul_kernel<M, KPM, BF, NOP, S, MINB>, kWsT,
+                                                      smem) != cudaSuccess ||
+        occ_emu < 1)
+      occ_emu = 1;
+    attr = true;
+  }
+  cudaError_t e;
+  if (!emu) {
+    int64_t grid = static_cast<int64_t>(ws_sms()) * occ;  // every CTA co-resident
+    if (T.max_ctas > 0) grid = std::min<int64_t>(grid, T.max_ctas);
+    grid = std::max<int64_t>(1, std::min<int64_t>(grid, static_cast<int64_t>(T.nparts) * kXLanes));
+    xgpu_ws_kernel<M, KPM, BF, NOP, S, MINB><<<static_cast<int>(grid), kWsT, smem, stream>>>(T);
+    e = cudaGetLastError();
+  } else {
+    const int64_t per =
+        std::min<int64_t>(static_cast<int64_t>(ws_sms()) * occ_emu / V, static_cast<int64_t>(max_parts) * kXLanes);
+    if (per < 1) {
+      *err = "xgpu_ws emulation: more virtual GPUs than resident CTAs";
+      return RP_EINVAL;
+    }
+    auto fn = xgpu_ws_emul_kernel<M, KPM, BF, NOP, S, MINB>;
+    void* args[] = {const_cast<XTask**>(&d_tasks), &V};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(static_cast<unsigned>(per * V)),
+                                    dim3(kWsT), args, smem, stream);
+  }
+  if (e != cudaSuccess) {
+    *err = std::string("xgpu_ws launch: ") + cudaGetErrorString(e);
+    return RP_ECUDA;
+  }
+  return RP_OK;
+}
+
+}  // namespace
+
+// Operand slots per stage: A needs 2M (x, g of every local member), B 2M + kp - 1 (+ the peers'
+// staged partials), C 1. Stages are sized so that two CTAs fit an SM where possible.
+int launch_xgpu_ws(XTask& T, const XTask* d_tasks, int V, int max_parts, void* stream, std::string* err, int mmax,
+                   int kpmax, bool emu) {
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (T.blag < 2) {
+    *err = "xgpu_ws: blag < 2";
+    return RP_EINVAL;
+  }
+#define RP_WS(M, KPM, BF, S, MINB) \
+  return launch_ws_m<M, KPM, BF, 2 * M + KPM - 1, S, MINB>(T, d_tasks, V, max_parts, s, err, emu)
+  const bool bf = T.bf16 != 0;
+  (void)emu;  // emulation takes the same instantiation as the real launch
+  if (kpmax <= 2) {
+    if (mmax <= 1) { if (bf) RP_WS(1, 2, true, 4, 2); RP_WS(1, 2, false, 4, 2); }
+    if (mmax <= 2) { if (bf) RP_WS(2, 2, true, 2, 2); RP_WS(2, 2, false, 2, 2); }
+    if (mmax <= 4) { if (bf) RP_WS(4, 2, true, 2, 1); RP_WS(4, 2, false, 2, 1); }
+    if (bf) RP_WS(8, 2, true, 1, 1);
+    RP_WS(8, 2, false, 1, 1);
+  }
+  if (kpmax <= 4) {
+    if (mmax <= 1) { if (bf) RP_WS(1, 4, true, 2, 2); RP_WS(1, 4, false, 2, 2); }
+    if (mmax <= 2) { if (bf) RP_WS(2, 4, true, 3, 1); RP_WS(2, 4, false, 3, 1); }
+    if (mmax <= 4) { if (bf) RP_WS(4, 4, true, 2, 1); RP_WS(4, 4, false, 2, 1); }
+    if (bf) RP_WS(8, 4, true, 1, 1);
+    RP_WS(8, 4, false, 1, 1);
+  }
+  if (mmax <= 1) { if (bf) RP_WS(1, 8, true, 2, 1); RP_WS(1, 8, false, 2, 1); }
+  if (mmax <= 2) { if (bf) RP_WS(2, 8, true, 2, 1); RP_WS(2, 8, false, 2, 1); }
+  if (bf) RP_WS(8, 8, true, 1, 1);
+  RP_WS(8, 8, false, 1, 1);
+#undef RP_WS
+}
+
+}  // namespace rp

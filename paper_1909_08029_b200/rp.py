@@ -29,6 +29,7 @@ RP_FLAG_SHARED_GG = 0x4
 RP_FLAG_RANDOM_GG = 0x8
 RP_FLAG_INTER_INTRA = 0x10
 RP_FLAG_EMULATE = 0x20
+RP_FLAG_GRAPH = 0x40
 RP_DTYPE_F32 = 0
 RP_DTYPE_BF16 = 1
 RP_SCHED_PAPER4 = 1

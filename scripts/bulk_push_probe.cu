@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #define CK(x)                                                                         \
@@ -119,6 +120,39 @@ __global__ void __launch_bounds__(T) push(const float4* __restrict__ x, const fl
   }
 }
 
+// granularity: each 16 KB tile pushed as `split` bulk stores of 16/split KB (issued by thread 0)
+__global__ void __launch_bounds__(T) push_split(const float4* __restrict__ x, const float4* __restrict__ g,
+                                                float4* dst, long n4, int split) {
+  extern __shared__ float4 sm[];
+  const long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long lo = blockIdx.x * per, hi = min(lo + per, n4);
+  int slot = 0;
+  for (long t0 = lo; t0 < hi; t0 += TILE) {
+    if (threadIdx.x == 0) wait_read<2>();
+    __syncthreads();
+    float4* b = sm + (slot % 3) * TILE;
+    ++slot;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      long i = t0 + r * T + threadIdx.x;
+      if (i < hi) {
+        float4 a = __ldcs(x + i), gg = __ldcs(g + i);
+        b[r * T + threadIdx.x] = make_float4(a.x - 0.1f * gg.x, a.y - 0.1f * gg.y, a.z - 0.1f * gg.z, a.w - 0.1f * gg.w);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long cnt = min(static_cast<long>(TILE), hi - t0);
+      const long piece = (cnt + split - 1) / split;
+      for (long q = 0; q < cnt; q += piece)
+        bulk_store(dst + t0 + q, b + q, static_cast<unsigned>(min(piece, cnt - q) * 16));
+      commit();
+    }
+  }
+  if (threadIdx.x == 0) wait_all();
+}
+
 int main() {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
@@ -143,6 +177,37 @@ int main() {
     CK(cudaFuncSetAttribute(push<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TILE * 16));
     CK(cudaFuncSetAttribute(push<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * TILE * 16));
   }
+  CK(cudaSetDevice(0));
+  CK(cudaFuncSetAttribute(push_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TILE * 16));
+  CK(cudaSetDevice(1));
+  CK(cudaFuncSetAttribute(push_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TILE * 16));
+  for (int split : {1, 2, 4, 8, 16, 32}) {
+    float best = 1e9f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEvent_t e0[2], e1[2];
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaSetDevice(i));
+        CK(cudaEventCreate(&e0[i]));
+        CK(cudaEventCreate(&e1[i]));
+        CK(cudaEventRecord(e0[i], st[i]));
+        push_split<<<296, T, 3 * TILE * 16, st[i]>>>(x[i], g[i], d[1 - i], n4, split);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(e1[i], st[i]));
+      }
+      float ms = 0;
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaSetDevice(i));
+        CK(cudaEventSynchronize(e1[i]));
+        float m = 0;
+        CK(cudaEventElapsedTime(&m, e0[i], e1[i]));
+        ms = m > ms ? m : ms;
+      }
+      if (rep > 0 && ms < best) best = ms;
+    }
+    printf("granularity: 16 KB tile as %2d bulk stores of %5.2f KB  %7.1f GB/s per direction (grid 296, no flags)\n",
+           split, 16.0 / split, bytes / (best * 1e-3) / 1e9);
+  }
+  if (getenv("PROBE_ONLY_SPLIT")) return 0;
   const char* names[] = {"no flags", "drain+fence+flag", "deferred fence+flag", "deferred release-only",
                          "plain STG drain"};
   for (int nbuf : {3, 4}) {

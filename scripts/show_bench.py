@@ -11,6 +11,9 @@ for f in sys.argv[1:]:
         continue
     r = d.get("roofline") or {}
     o = r.get("other_kernel") or {}
+    x = r if r.get("bound") == "nvlink" else o
+    sl = (x.get("step_level") or {}).get("frac")
+    kl = (x.get("kernel_level") or {}).get("frac")
     print(f"{f}: {d.get('impl')} value={d['value']} ms/step={d['ms_per_step']} "
           f"roof={r.get('bound')}:{r.get('achieved')}({r.get('frac')}) other={o.get('bound')}:{o.get('achieved')} "
-          f"busbw={d.get('busbw_gbs')}")
+          f"nvlink kernel-level={kl} step-level={sl} busbw={d.get('busbw_gbs')}")

@@ -10,10 +10,33 @@ import numpy as np
 KIND = {0: "A", 1: "B", 2: "C"}
 
 
+def cta_breakdown(path):
+    """RP_XGPU_PROFILE=path also dumps path.cta.<rank>: per CTA ns [ring wait, signal wait, flag wait, total]."""
+    import os
+    base, rank = path.rsplit(".", 1)
+    p = f"{base}.cta.{rank}"
+    if not os.path.exists(p):
+        return
+    a = np.fromfile(p, dtype=np.uint64).reshape(-1, 4).astype(np.float64)
+    a = a[a[:, 3] > 0]
+    if not len(a):
+        return
+    tot = a[:, 3].sum()
+    ring, sig, flag = (a[:, i].sum() / tot for i in range(3))
+    print(f"  per-CTA time ({len(a)} CTAs, mean total {a[:, 3].mean() / 1e3:.1f} us): [0] {ring:.1%}, [1] {sig:.1%}, "
+          f"[2] peer-flag wait {flag:.1%}, rest {1 - ring - sig - flag:.1%}  (register kernel: [0] smem-ring wait, [1] "
+          f"signal wait; warp-specialized kernel: [0] consumer warp 0 waiting for loaded data, [1] its signal wait, "
+          f"[2] the producer's flag waits)")
+
+
 def main():
     for path in sys.argv[1:]:
+        cta_breakdown(path)
         rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 4)
         rec = rec[rec[:, 0] > 0]
+        if not len(rec):  # the warp-specialized kernel records only the per-CTA breakdown
+            print(f"== {path}: no item records")
+            continue
         t0 = rec[:, 0].min()
         ts, tr, te = [(rec[:, i] - t0).astype(np.float64) / 1e3 for i in range(3)]  # us
         kind = (rec[:, 3] >> np.uint64(62)).astype(int)

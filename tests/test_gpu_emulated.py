@@ -91,3 +91,72 @@ def test_emulated_full_r50_sampled():
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     _run(4, 1, N_R50, 3, "gd", None, 3, {"native": True}, sample=4099)
+
+
+def test_emulated_r50x8_100_steps():
+    # the bench's default problem (8 workers, ResNet-50 size, k = 3, GB + GD) on 2 virtual GPUs
+    # through rp_lockstep_run for 100 steps (the north star's 100-step bar), sampled slices
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    _run(2, 4, N_R50, 3, "gd", None, 100, {"native": True}, sample=4099)
+
+
+def test_emulated_rerun_same_steps_after_reinit():
+    # a re-run of the same step numbers on the same context (runner.init_replicas resets t to 0)
+    # must not meet stale flags of the first run: tags are unique per (group launch, GPU pair)
+    # (round-1 advice: static-schedule tags were a function of (step, lowest member) only)
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1909_08029_b200.runner import LockstepRunner
+    n, T = 200_003, 6
+    r = LockstepRunner(4, n, mode="static", rule="shift_k", group_size=3, n_gpus=2, device=0, emulate=True)
+    r.run(T)
+    r.init_replicas()
+    r.run(T)
+    r.synchronize()
+    X, _ = sim.run_lockstep(4, n, T, mode="static", rule="shift_k", k=3, workers_per_gpu=2)
+    for w in range(4):
+        got = r.x(w).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), X[w].view(np.uint32)), w
+    r.ctx.check()
+    r.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_emulated_non_finite_gradients(dtype):
+    # a NaN / inf gradient element: the cross-GPU path must keep NaN a NaN (round-1 advice: the
+    # bf16 push path rounded NaN to -0.0) and propagate inf like the oracle (reading R26 for bf16)
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from oracle import update as U
+    from paper_1909_08029_b200.runner import LockstepRunner
+    from rp_inputs import gen
+    n, T, lr = 5003, 3, np.float32(0.1)
+    r = LockstepRunner(2, n, mode="static", rule="shift_k", group_size=2, n_gpus=2, device=0, emulate=True,
+                       dtype=dtype)
+    G = {w: gen.grad(w, 1, n) for w in range(2)}
+    G[0][17] = np.nan
+    G[1][4000] = np.inf
+    G[1][4001] = -np.nan
+    if dtype == "bf16":
+        G = {w: U.bf16_round(v) for w, v in G.items()}
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    grads = {w: torch.from_numpy(G[w]).to(tdt).to("cuda:0") for w in range(2)}
+    for _ in range(T):
+        r.step(grads)
+    r.synchronize()
+    X = {w: gen.x0(w, n) for w in range(2)}
+    if dtype == "bf16":
+        X = {w: U.bf16_round(v) for w, v in X.items()}
+    for _ in range(T):
+        if dtype == "bf16":
+            U.fused_group_update_bf16(X, G, (0, 1), lr, 1)
+        else:
+            U.fused_group_update(X, G, (0, 1), lr, 1)
+    for w in range(2):
+        got = r.x(w).float().cpu().numpy()
+        nan = np.isnan(X[w])
+        assert np.array_equal(np.isnan(got), nan), w
+        assert nan[17] and nan[4001]
+        assert np.array_equal(got[~nan].view(np.uint32), X[w][~nan].view(np.uint32)), w
+    r.close()

@@ -122,19 +122,29 @@ def test_multi_gpu_nvls_parity(gpus, spec):
 
 
 @pytest.mark.parametrize("gpus,split,spec", [
-    # fused mode (intra-GPU groups as L items of the cross launch) and a capped cross grid
+    # RP_XGPU_SPLIT caps the cross launch's grid beside a concurrent intra-GPU launch; uncapped (0)
+    # and capped grids on different GPUs must still agree on every chunk flag (the chunk
+    # geometry depends on n and kp only)
     (2, "0", dict(wpg=4, n=50_007, k=3, mode="gd", steps=8, ii=True)),
     (2, "0", dict(wpg=4, n=100_003, k=3, mode="gd", steps=12)),
     (2, "37", dict(wpg=4, n=50_007, k=3, mode="gd", steps=8, ii=True)),
     (4, "37", dict(wpg=8, n=30_011, k=3, mode="gd", steps=8, ii=True)),
 ])
 def test_multi_gpu_split_modes(gpus, split, spec):
-    # RP_XGPU_SPLIT: a GPU whose step has ONE cross part runs its intra-GPU groups beside the
-    # cross launch (default); 0 = fused L items; a cap must not change the chunk geometry
-    # (peers with different caps must still agree on every chunk flag)
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, {"sample": 0, "rule": None, **spec}, env={"RP_XGPU_SPLIT": split})
+
+
+@pytest.mark.parametrize("gpus,env,spec", [
+    # geometry knobs (RP_XGPU_ITERS / RP_XGPU_MIN_TILES): one lane iteration, many small chunks
+    (2, {"RP_XGPU_ITERS": "1"}, dict(wpg=2, n=300_007, k=3, mode="static", rule="shift_k", steps=8)),
+    (2, {"RP_XGPU_ITERS": "16", "RP_XGPU_MIN_TILES": "1"}, dict(wpg=4, n=3_000_017, k=3, mode="gd", steps=8)),
+])
+def test_multi_gpu_geometry_knobs(gpus, env, spec):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, **spec}, env=env)
 
 
 BF16_CASES = [
@@ -165,6 +175,10 @@ def test_multi_gpu_bf16_parity(gpus, spec):
     (2, dict(wpg=2, n=100_003, k=3, mode="static", rule="shift_k", steps=10)),
     (4, dict(wpg=8, n=30_011, k=3, mode="gd", steps=8, ii=True)),
     (4, dict(wpg=1, n=200_003, k=3, mode="gd", steps=10, dtype="bf16")),
+    # the bench's default problem at N = 2 (8 workers, ResNet-50 size, GB + GD), 100 steps
+    (2, dict(wpg=4, n=N_R50, k=3, mode="gd", steps=100, sample=4099)),
+    # configs[2] at N = 4 (kp = 3 groups), 100 steps
+    (4, dict(wpg=1, n=N_R50, k=3, mode="gd", steps=100, sample=4099)),
 ])
 def test_multi_gpu_native_executor(gpus, spec):
     if _ngpu() < gpus:
