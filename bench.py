@@ -371,6 +371,9 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
     per_rank = D.gather({"recs": recs, "launches": launches, "clocks": clk.summary(), "gpm": g,
                          "hbm": st1["bytes_hbm"] - st0["bytes_hbm"], "nvl": st1["bytes_nvlink"] - st0["bytes_nvlink"],
                          "cross": st1["cross_gpu_groups"] - st0["cross_gpu_groups"]})
+    if os.environ.get("RP_BENCH_DUMP_RECS") and rank == 0:   # debugging: every rank's per-launch records
+        with open(os.environ["RP_BENCH_DUMP_RECS"], "w") as f:
+            json.dump([r["recs"] for r in per_rank], f)
     e2e_line = run_e2e(runner, args, D, step_fn) if e2e else None
     runner.close()
     del runner
@@ -539,7 +542,7 @@ class BaselineState:
     """Replicas / gradients of this rank's workers + the seeded schedule (host-only librp context:
     the same static rule or the same replicated GG as ours, so both arms run the same groups)."""
 
-    def __init__(self, wl, D, delay_ns=0):
+    def __init__(self, wl, D, delay_ns=0, alloc=True):
         import torch
         from paper_1909_08029_b200 import rp
         self.rp, self.D = rp, D
@@ -547,6 +550,11 @@ class BaselineState:
         self.world = self.wpg * D.n
         self.k = min(wl["k"], self.world)
         self.wl = wl
+        self.t = 0
+        nodes = D.n if wl["rule"] == "paper4" else 0
+        self.host = rp.Context(self.world, self.n, n_gpus=0, group_size=self.k, c_thres=4, nodes=nodes, seed_gd=3)
+        if not alloc:
+            return
         ld = (self.n + 63) // 64 * 64
         self.X = torch.empty((self.wpg, ld), device="cuda")
         self.G = torch.empty((self.wpg, ld), device="cuda")
@@ -556,10 +564,7 @@ class BaselineState:
         for i, w in enumerate(self.local):
             rp.fill_xi(self.X[i], self.n, 1, w, 0, 0, s)
             rp.fill_xi(self.G[i], self.n, 2, w, 1, 0, s)
-        nodes = D.n if wl["rule"] == "paper4" else 0
-        self.host = rp.Context(self.world, self.n, n_gpus=0, group_size=self.k, c_thres=4, nodes=nodes, seed_gd=3)
         self.delay_ns = delay_ns
-        self.t = 0
 
     def x(self, w):
         return self.X[self.local.index(w), :self.n]
@@ -656,10 +661,24 @@ def run_nccl_group(args, wl, name, D, steps=None, warmup=None):
     import torch
     import torch.distributed as dist
     steps, warmup = steps or args.steps, warmup or args.warmup
+    # the schedule of the whole run (a second host-only GG with the same seed): the GPU subsets
+    # of its cross-GPU groups, in order of first use. The paper keeps <= 64 communicators
+    # cached, so the warm state is every subset the run needs, up to 64; they are created
+    # (ncclCommSplit) and connected (one small all-reduce each) before timing. A run needing
+    # more than 64 subsets evicts inside the timed region, as the paper's cache would.
+    P = BaselineState(wl, D, alloc=False)
+    order = []
+    for _ in range(warmup + steps):
+        for g in P.groups():
+            gpus = tuple(sorted({w // P.wpg for w in g}))
+            if len(gpus) > 1 and gpus not in order:
+                order.append(gpus)
+    P.close()
     B = BaselineState(wl, D)
     s = torch.cuda.current_stream().cuda_stream
     cache = collections.OrderedDict()
-    stats = {"created": 0, "evicted": 0}
+    stats = {"created": 0, "evicted": 0, "subsets_in_run": len(order)}
+    probe = torch.zeros(1024, device="cuda")
 
     def comm(gpus):
         if gpus in cache:
@@ -672,6 +691,13 @@ def run_nccl_group(args, wl, name, D, steps=None, warmup=None):
         cache[gpus] = dist.new_group(ranks=list(gpus), backend="nccl")   # collective: all ranks, same order
         stats["created"] += 1
         return cache[gpus]
+
+    for gpus in order[:64]:                  # warm cache: create + connect
+        pg = comm(gpus)
+        if D.rank in gpus:
+            dist.all_reduce(probe, group=pg)
+    torch.cuda.synchronize()
+    stats["created_before_timing"] = stats["created"]
 
     def step():
         for g in B.groups():

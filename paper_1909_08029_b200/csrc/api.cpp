@@ -276,7 +276,8 @@ cudaEvent_t timing_event(rp_ctx* c) {
 // local (caller holds mu). The kernel runs on the stream of the lowest local
 // member after every member's arrival event; every member's stream is then
 // ordered after the kernel and records its own completion event.
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream, int max_ctas = 0);
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs, cudaStream_t stream, int max_ctas = 0,
+                 const std::vector<int64_t>& local = {});
 int launch_nvls_groups(rp_ctx* c, std::vector<int64_t> seqs, cudaStream_t stream);
 int pump_cross(rp_ctx* c);
 
@@ -348,6 +349,39 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
   if (split_order < 0) {
     const char* v = std::getenv("RP_SPLIT_ORDER");
     split_order = v && *v ? std::atoi(v) : 0;
+  }
+  // Fusion (default; RP_XGPU_FUSE=0 disables): intra-GPU groups of <= 4 members (<= 16 groups) ride
+  // in the cross launch as L jobs of the warp-specialized kernel, spread over its lane iterations
+  // (their HBM work fills the time NVLink flag waits leave idle; a concurrent launch could not
+  // co-reside with the cross kernel's shared memory anyway). Momentum steps take the register
+  // kernel, which has no L jobs: they keep the separate launch.
+  static int fuse_env = -1;
+  if (fuse_env < 0) {
+    const char* v = std::getenv("RP_XGPU_FUSE");
+    fuse_env = v && *v ? std::atoi(v) : 1;
+  }
+  std::vector<int64_t> fused;
+  if (fuse_env && !cross.empty() && nv.empty() && !seqs.empty() && split_order == 0) {
+    bool ok = seqs.size() <= static_cast<size_t>(rp::kMaxXLocalGroups);
+    for (int64_t q : seqs) {
+      const ActiveGroup& a = c->active.at(q);
+      ok = ok && a.g.size <= rp::kMaxFusedK;
+      for (int i = 0; i < a.g.size; ++i) ok = ok && !(a.u[i].v && a.u[i].g);
+    }
+    for (int64_t q : cross) {
+      const ActiveGroup& a = c->active.at(q);
+      for (int i = 0; i < a.g.size; ++i) ok = ok && !(a.u[i].v && a.u[i].g);
+    }
+    // ... unless the intra-GPU work dominates the step (more than twice the cross part's local
+    // members, e.g. the Inter step of Inter-Intra with one Head Worker per GPU): the dedicated
+    // dynamic-tile kernel moves bulk HBM traffic faster than L jobs between lane iterations
+    // (cfg2ii at N = 2: 33.5k fused vs 36.0k separate; cfg4: 4.0k fused vs 3.4k separate,
+    // profiles/r02/sweep_fuse_2gpu.txt)
+    int intra_members = 0, cross_members = 0;
+    for (int64_t q : seqs) intra_members += c->active.at(q).g.size;
+    for (int64_t q : cross) cross_members += __builtin_popcountll(c->active.at(q).local_mask);
+    if (c->emulate) cross_members = intra_members;  // emulation: always exercise the L jobs
+    if (ok && intra_members <= 2 * cross_members) fused.swap(seqs);
   }
   const bool split = !cross.empty() && nv.empty() && !seqs.empty() && !c->emulate && c->aux && c->xs &&
                      split_order == 0;
@@ -429,7 +463,7 @@ int launch_groups(rp_ctx* c, const std::vector<int64_t>& all_seqs) {
     if (rc != RP_OK) return rc;
   }
   if (!split && !cross.empty()) {
-    const int rc = launch_cross(c, cross, L.stream);
+    const int rc = launch_cross(c, cross, L.stream, 0, fused);
     if (rc != RP_OK) return rc;
   }
   CUDA_TRY(cudaEventRecord(L.ev_group, L.stream));
@@ -463,8 +497,8 @@ float* replica_of(rp_ctx* c, int m) {
 
 // GPU `gpu`'s parts of the cross-GPU groups `seqs` (ascending seq: the same part order on every
 // GPU), with the algorithmic bytes of those parts (caller holds mu).
-int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, int gpu, rp::XTask& T, int64_t* nvl_out,
-               int64_t* hbm_out) {
+int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<int64_t>& local, int gpu,
+               rp::XTask& T, int64_t* nvl_out, int64_t* hbm_out) {
   const int wpg = c->cfg.workers_per_gpu;
   T = rp::XTask{};
   T.my_gpu = gpu;
@@ -518,6 +552,19 @@ int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, int gpu, rp::XTask& 
     // A+B reads of x,g; B reads of staged partials; B stores of xbar; C copies (m > 1)
     hbm += rd * T.n + 4 * (p.kp - 1) * mine + esz * p.m * mine + 2 * esz * (p.m - 1) * others;
   }
+  for (int64_t q : local) {  // fused intra-GPU groups of this GPU (L jobs)
+    ActiveGroup& a = c->active.at(q);
+    if (a.g.members[0] / wpg != gpu) continue;
+    rp::XLocalGroup& G = T.lg[T.nlocal++];
+    G.k = a.g.size;
+    for (int i = 0; i < a.g.size; ++i) {
+      G.x[i] = c->w[a.g.members[i]].x;
+      G.u[i] = a.u[i];
+      hbm += member_bytes(a.u[i], T.bf16) * T.n;
+    }
+    c->stats.groups_launched++;
+    if (a.g.size == 1) c->stats.singleton_groups++;
+  }
   *nvl_out = nvl;
   *hbm_out = hbm;
   return RP_OK;
@@ -526,7 +573,8 @@ int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, int gpu, rp::XTask& 
 // This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch (caller holds mu;
 // members' arrival events already joined into `stream`). Emulated GPUs: every virtual GPU's
 // parts in ONE cooperative launch.
-int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t stream, int max_ctas) {
+int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t stream, int max_ctas,
+                 const std::vector<int64_t>& local) {
   if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
   std::vector<int64_t> seqs(seqs_in);
   std::sort(seqs.begin(), seqs.end());
@@ -547,7 +595,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
     std::vector<rp::XTask> tasks(V);
     for (int d = 0; d < V; ++d) {
       int64_t a = 0, b = 0;
-      const int rc = build_task(c, seqs, d, tasks[d], &a, &b);
+      const int rc = build_task(c, seqs, local, d, tasks[d], &a, &b);
       if (rc != RP_OK) return rc;
       nvl += a;
       hbm += b;
@@ -556,7 +604,7 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
     if (rc != RP_OK) return fail(rc, err);
   } else {
     rp::XTask T;
-    int rc = build_task(c, seqs, c->cfg.rank, T, &nvl, &hbm);
+    int rc = build_task(c, seqs, local, c->cfg.rank, T, &nvl, &hbm);
     if (rc != RP_OK) return rc;
     T.max_ctas = max_ctas;
     if (!c->prof_path.empty()) {

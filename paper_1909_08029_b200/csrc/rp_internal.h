@@ -146,6 +146,16 @@ struct XErr {
   unsigned long long tag, seen;
 };
 
+// Intra-GPU groups of the same step fused into the cross-GPU launch as "L jobs" of the
+// warp-specialized kernel, so their HBM-only work fills the time the NVLink transfers leave.
+constexpr int kMaxXLocalGroups = 16;
+constexpr int kMaxFusedK = 4;
+struct XLocalGroup {
+  int32_t k;
+  float* x[kMaxFusedK];
+  MemberUpdate u[kMaxFusedK];
+};
+
 // Kernel parameters exceed 4 KB: CUDA >= 12.1 large-parameter launches (sm_70+).
 struct XTask {
   int32_t nparts;
@@ -160,6 +170,8 @@ struct XTask {
   int32_t nbuf;                            // shared-memory tile ring depth (launcher)
   int32_t blag;                            // warp-specialized kernel: B runs blag (>= 2) iterations after A
   unsigned long long* cta_stat;            // profiling: per CTA ns [ring wait, signal wait, flag wait, total]
+  int32_t nlocal;                          // fused intra-GPU groups (warp-specialized kernel only)
+  XLocalGroup lg[kMaxXLocalGroups];
   XPart part[kMaxXParts];
 };
 
@@ -171,6 +183,8 @@ void xgpu_geometry(XPart& p, int64_t n);
 int64_t xgpu_stage_region_bytes(int64_t n);
 // This GPU's parts of the cross-GPU groups of one step, in ONE launch.
 int launch_xgpu(XTask& t, void* stream, std::string* err);
+// RP_XGPU_V2=1: plain-SGD steps take the register kernel of xgpu.cu instead (comparison)
+bool use_v2();
 // The warp-specialized cross-GPU kernel (xgpu_ws.cu; plain SGD, fp32 and bf16): TMA bulk loads
 // into a staged ring, bulk stores out. emu: d_tasks holds V uploaded tasks (cooperative launch).
 int launch_xgpu_ws(XTask& T, const XTask* d_tasks, int V, int max_parts, void* stream, std::string* err, int mmax,

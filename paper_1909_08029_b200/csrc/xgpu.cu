@@ -815,6 +815,29 @@ int check_task(const XTask& T, int* mmax, int* kpmax, bool* mom, std::string* er
     *err = "xgpu: bf16 replicas take plain SGD";
     return RP_EINVAL;
   }
+  if (T.nlocal < 0 || T.nlocal > kMaxXLocalGroups) {
+    *err = "xgpu: bad fused-group count";
+    return RP_EINVAL;
+  }
+  for (int gi = 0; gi < T.nlocal; ++gi) {
+    const XLocalGroup& G = T.lg[gi];
+    if (G.k < 1 || G.k > kMaxFusedK) {
+      *err = "xgpu: fused intra-GPU groups have 1..4 members";
+      return RP_EINVAL;
+    }
+    for (int m = 0; m < G.k; ++m) {
+      if (!G.x[m] || (reinterpret_cast<uintptr_t>(G.x[m]) & 15) || (reinterpret_cast<uintptr_t>(G.u[m].g) & 15)) {
+        *err = "xgpu: fused group replica / gradient pointers must be non-null and 16-byte aligned";
+        return RP_EINVAL;
+      }
+      *mom = *mom || (G.u[m].v && G.u[m].g);
+    }
+    *mmax = std::max(*mmax, static_cast<int>(G.k));  // L jobs need 2k operand slots (2M >= 2k)
+  }
+  if (T.nlocal > 0 && (*mom || use_v2())) {
+    *err = "xgpu: fused intra-GPU groups need the warp-specialized kernel (plain SGD, RP_XGPU_V2 unset)";
+    return RP_EINVAL;
+  }
   return RP_OK;
 }
 
@@ -823,7 +846,7 @@ int check_task(const XTask& T, int* mmax, int* kpmax, bool* mom, std::string* er
 // RP_XGPU_V2=1: the register (LDG/STG) version of this file for plain SGD too (comparison);
 // momentum steps always take it (their buffers are read and written per member)
 int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stages (tuning)
-  static const int v = std::max(2, std::min(6, env_int("RP_XGPU_BLAG", 2)));
+  static const int v = std::max(2, std::min(6, env_int("RP_XGPU_BLAG", 3)));  // 3: profiles/r02/sweep_blag_2gpu.txt
   return v;
 }
 

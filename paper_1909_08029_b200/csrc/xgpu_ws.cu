@@ -42,7 +42,7 @@ constexpr int kPW = kT / kWarps;                // vectors per consumer warp and
 constexpr int kVPL = kPW / 32;                  // vectors per lane and tile
 constexpr int kGeomTile = 1024;                 // xgpu.cu's chunk / slice alignment (vectors)
 constexpr int kSigRing = 8;                     // SIG counters (> max stages)
-constexpr int kJA = 0, kJB = 1, kJC = 2, kJSig = 3, kJEnd = 4;
+constexpr int kJA = 0, kJB = 1, kJC = 2, kJSig = 3, kJEnd = 4, kJL = 5;
 
 struct Job {                // one stage's work, written by the producer next to the stage
   int32_t kind, pi, o, cnt;
@@ -225,6 +225,85 @@ constexpr size_t ws_smem() {
 }
 
 // ---- consumer side ----
+// L job: tile of a fused intra-GPU group (alg1 steps 2 + 4 on one GPU, pinned fold, reading R1);
+// operand slots 2m / 2m+1 hold x_m / g_m; the mean goes to every member by bulk stores (HBM)
+template <bool BF>
+__device__ __forceinline__ void consume_L(const XTask& T, const Job& J, const float4* st, float4* out, int ob, int warp,
+                                          int lane, int& ncommit) {
+  const XLocalGroup& G = T.lg[J.pi];
+  const int e0 = warp * kPW;
+  const int mine = max(0, min(kPW, J.cnt - e0));
+#pragma unroll
+  for (int j = 0; j < kVPL; ++j) {
+    const int e = e0 + j * 32 + lane;
+    if (e >= J.cnt) continue;
+    const int64_t i = J.base + e;
+    const bool odd_last = BF && (J.cnt & 1) && e == J.cnt - 1;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < kMaxFusedK; ++m) {
+      if (m >= G.k) break;
+      float4 x, g, vd;
+      if constexpr (BF) {
+        if (odd_last) {
+          x = unpack_bf4(*reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(G.x[m]) + 4 * i));
+          if (G.u[m].g) g = unpack_bf4(*reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(G.u[m].g) + 4 * i));
+        } else {
+          x = unpack_bf4(reinterpret_cast<const uint2*>(st + (2 * m) * kT)[e]);
+          if (G.u[m].g) g = unpack_bf4(reinterpret_cast<const uint2*>(st + (2 * m + 1) * kT)[e]);
+        }
+      } else {
+        x = st[(2 * m) * kT + e];
+        if (G.u[m].g) g = st[(2 * m + 1) * kT + e];
+      }
+      const float4 y = step4<false>(x, g, vd, G.u[m]);
+      s = m == 0 ? y : add4(s, y);
+    }
+    if (G.k > 1) s = div4(s, static_cast<float>(G.k));
+    if constexpr (BF) {
+      reinterpret_cast<uint2*>(out + ob * kT)[e] = pack_bf4(s);
+      if (odd_last)
+        for (int m = 0; m < G.k; ++m)
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(G.x[m]) + 4 * i) = pack_bf4(s);
+    } else {
+      out[ob * kT + e] = s;
+    }
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0 && mine > 0) {
+    int nb = mine;
+    if (BF && (J.cnt & 1) && e0 + mine == J.cnt) nb = mine - 1;
+    const uint32_t bytes = static_cast<uint32_t>(nb * (BF ? 8 : 16));
+    const int64_t off = BF ? 8 * (J.base + e0) : 16 * (J.base + e0);
+    const char* srcb = reinterpret_cast<const char*>(BF ? static_cast<const void*>(reinterpret_cast<const uint2*>(out + ob * kT) + e0)
+                                                       : static_cast<const void*>(out + ob * kT + e0));
+    if (bytes)
+      for (int m = 0; m < G.k; ++m) bulk_store(reinterpret_cast<char*>(G.x[m]) + off, srcb, bytes);
+  }
+  if (lane == 0) {
+    bulk_commit();
+    ++ncommit;
+  }
+}
+
+template <bool BF>
+__device__ __forceinline__ void tail_L(const XTask& T, int gi, int lane) {
+  const XLocalGroup& G = T.lg[gi];
+  const int64_t n4 = T.n / 4;
+  const int rem = static_cast<int>(T.n - 4 * n4);
+  if (lane >= rem) return;
+  const int64_t j = 4 * n4 + lane;
+  float s = 0.f;
+  for (int m = 0; m < G.k; ++m) {
+    float y = ldx1<BF>(G.x[m], j);
+    if (G.u[m].g) y = step_sgd(y, ldx1<BF>(G.u[m].g, j), G.u[m].lr);
+    s = m == 0 ? y : __fadd_rn(s, y);
+  }
+  if (G.k > 1) s = __fdiv_rn(s, static_cast<float>(G.k));
+  for (int m = 0; m < G.k; ++m) stx1<BF>(G.x[m], j, s);
+}
+
 template <int M, int KPM, bool BF>
 __device__ __forceinline__ void consume(const XTask& T, const Job& J, const float4* st, float4* out, int ob, int warp,
                                         int lane, int& ncommit) {
@@ -434,6 +513,42 @@ __device__ void produce_tiles(const XTask& T, int pi, int kind, int o, int64_t c
   }
 }
 
+// L tile q of this launch (group q mod nlocal, tile q / nlocal): x and g of every member
+template <bool BF, int NOP, int S>
+__device__ void produce_L(const XTask& T, int64_t q, float4* stages, uint64_t* full, uint64_t* empty, Job* jobs,
+                          Prod& P) {
+  const int64_t n4 = T.n / 4;
+  const int64_t tiles = (n4 + kT - 1) / kT;
+  const int gi = static_cast<int>(q % T.nlocal);
+  const int64_t ti = q / T.nlocal;
+  const XLocalGroup& G = T.lg[gi];
+  const int64_t t0 = ti * kT;
+  const int cnt = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(kT), n4 - t0)));
+  const int s = acquire_stage<NOP, S>(P, empty);
+  Job& J = jobs[s];
+  J.kind = kJL;
+  J.pi = gi;
+  J.o = 0;
+  J.cnt = cnt;
+  J.base = t0;
+  J.tail = (ti == max(tiles, static_cast<int64_t>(1)) - 1) && T.n > 4 * n4;
+  float4* st = stages + static_cast<size_t>(s) * NOP * kT;
+  const uint32_t xb = static_cast<uint32_t>(BF ? (cnt & ~1) * 8 : cnt * 16);
+  uint32_t tot = 0;
+  for (int m = 0; m < G.k; ++m) tot += G.u[m].g ? 2 * xb : xb;
+  if (tot == 0) {
+    mbar_arrive(&full[s]);
+  } else {
+    mbar_expect_tx(&full[s], tot);
+    const int64_t eo = BF ? 8 * t0 : 16 * t0;
+    for (int m = 0; m < G.k; ++m) {
+      bulk_load(st + (2 * m) * kT, reinterpret_cast<const char*>(G.x[m]) + eo, xb, &full[s]);
+      if (G.u[m].g) bulk_load(st + (2 * m + 1) * kT, reinterpret_cast<const char*>(G.u[m].g) + eo, xb, &full[s]);
+    }
+  }
+  advance<S>(P);
+}
+
 template <int NOP, int S>
 __device__ __forceinline__ void produce_marker(int kind, int pi, int64_t pA, int64_t pB, int sig, uint64_t* full,
                                                uint64_t* empty, Job* jobs, Prod& P) {
@@ -484,6 +599,21 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
       unsigned long long ready_seen = 0;
       int sig = 0;
       bool ok = true;
+      // fused intra-GPU groups: this CTA's L tiles q = cta, cta + ncta, ..., spread evenly over
+      // its lane iterations (they never wait, so they fill the time flag waits would idle)
+      const int64_t ltiles = T.nlocal > 0 ? T.nlocal * max(static_cast<int64_t>(1), (T.n / 4 + kT - 1) / kT) : 0;
+      int64_t lq = cta, iters_left = 0;
+      for (int idx = cta; idx < total; idx += ncta) {
+        const XPart& p = T.part[idx % T.nparts];
+        const int ln = idx / T.nparts;
+        const int64_t it = ln < p.nch ? (p.nch - 1 - ln) / kXLanes + 1 : 0;
+        iters_left += it ? it + 2 * T.blag : 0;
+      }
+      auto emit_L = [&](bool all) {
+        const int64_t left = lq < ltiles ? (ltiles - lq + ncta - 1) / ncta : 0;
+        int64_t want = all || iters_left <= 0 ? left : (left + iters_left - 1) / iters_left;
+        for (; want > 0 && lq < ltiles; --want, lq += ncta) produce_L<BF, NOP, S>(T, lq, stages, full, empty, jobs, P);
+      };
       for (int idx = cta; ok && idx < total; idx += ncta) {
         const int pi = idx % T.nparts, ln = idx / T.nparts;
         const XPart& p = T.part[pi];
@@ -523,11 +653,16 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
               fence_async_all();
               if (ok && p.m > 1) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJC, o, cC, stages, full, empty, jobs, P);
             }
-          if (ok) produce_marker<NOP, S>(kJSig, pi, pA, pB, sig++, full, empty, jobs, P);
+          if (ok) {
+            emit_L(false);
+            --iters_left;
+            produce_marker<NOP, S>(kJSig, pi, pA, pB, sig++, full, empty, jobs, P);
+          }
           pA = cA;
           pB = cB;
         }
       }
+      if (ok) emit_L(true);  // leftovers (and every L tile of a CTA without lane work)
       if (!ok) *reinterpret_cast<volatile int*>(abort_w) = 1;
       produce_marker<NOP, S>(kJEnd, 0, -1, -1, 0, full, empty, jobs, P);
     }
@@ -576,6 +711,14 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
       // the group that read out[ntile & 1] two tiles ago must have finished reading it
       if (lane == 0) bulk_wait_read1();
       __syncwarp();
+      if (J.kind == kJL) {
+        consume_L<BF>(T, J, st, out, ntile & 1, warp, lane, ncommit);
+        ++ntile;
+        if (J.tail && warp == 0) tail_L<BF>(T, J.pi, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
       consume<M, KPM, BF>(T, J, st, out, ntile & 1, warp, lane, ncommit);
       ++ntile;
       // the scalar tail rides on the chunk's last job (warp 0); the other warps release the stage
