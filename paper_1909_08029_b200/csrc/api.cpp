@@ -950,6 +950,21 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       return cuda_fail(e, "cudaSetDevice");
     }
     c->has_gpu = true;
+    {  // once per process and device: load every kernel now, not at a first launch in a timed region
+      static std::mutex pl_mu;
+      static uint64_t pl_done = 0;
+      std::lock_guard<std::mutex> pl(pl_mu);
+      if (!((pl_done >> k.device) & 1)) {
+        rp::preload_preduce();
+        rp::preload_preduce_tma();
+        if (k.n_gpus > 1) {
+          rp::preload_xgpu_ws();
+          rp::preload_xgpu();
+        }
+        cudaGetLastError();
+        pl_done |= 1ull << k.device;
+      }
+    }
     c->emulate = (k.flags & RP_FLAG_EMULATE) != 0;
     const int wpg = c->cfg.workers_per_gpu;
     const int w_lo = c->emulate ? 0 : k.rank * wpg, w_hi = c->emulate ? k.world : (k.rank + 1) * wpg;

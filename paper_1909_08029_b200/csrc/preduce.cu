@@ -219,6 +219,18 @@ int launch_kmax(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
 
 }  // namespace
 
+void preload_preduce() {  // every instantiation launch_preduce_multi can pick (see preload_xgpu_ws)
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<2, 2, 1, true>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<4, 1, 1, true>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<8, 1, 1, true>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<16, 1, 1, true>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<2, 2, 1, false>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<4, 2, 1, false>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<8, 1, 1, false>);
+  cudaFuncGetAttributes(&a, preduce_multi_kernel<16, 1, 1, false>);
+}
+
 int launch_preduce_multi(const MultiTask& t, int64_t n, void* stream, std::string* err) {
   if (t.ngroups < 1 || t.ngroups > kMaxTasks) {
     *err = "preduce: bad group count";

@@ -830,6 +830,27 @@ int launch_tma(MultiTask t, int64_t n, cudaStream_t stream, std::string* err) {
 }  // namespace
 
 // Returns RP_EINVAL (caller falls back to the LDG kernel) for shapes it does not cover.
+template <bool BF>
+void tma_touch() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, preduce_dyn_kernel<3, 256, 3, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_dyn_kernel<4, 256, 2, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_dyn_kernel<3, 256, 4, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_dyn_kernel<4, 256, 3, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_dyn_kernel<8, 256, 3, 1, BF>);
+  cudaFuncGetAttributes(&a, preduce_ws_kernel<3, 256, 4, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_ws_kernel<4, 256, 3, 2, BF>);
+  cudaFuncGetAttributes(&a, preduce_ws_kernel<8, 256, 3, 1, BF>);
+  cudaFuncGetAttributes(&a, preduce_ws_kernel<8, 256, 2, 1, BF>);
+  cudaFuncGetAttributes(&a, preduce_tma_kernel<16, 64, 6, 1, BF>);
+}
+
+// every default-path instantiation (variant 7 + its fallbacks; see preload_xgpu_ws)
+void preload_preduce_tma() {
+  tma_touch<false>();
+  tma_touch<true>();
+}
+
 int launch_preduce_tma(const MultiTask& t, int64_t n, void* stream, std::string* err, int variant, bool bf16) {
   int kmax = 0;
   int nm = 0;

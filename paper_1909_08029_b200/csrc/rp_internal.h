@@ -248,6 +248,12 @@ struct NTask {
 // This GPU's parts of every NVLS group of one step, in ONE launch (items P*, R*, S*).
 int launch_nvls(NTask& t, void* stream, std::string* err);
 int launch_delay(void* stream, int64_t ns, std::string* err);
+// Force-load the kernels each launcher can pick (CUDA lazy loading would load them at their first
+// launch, which a random schedule may reach only inside a timed region). Called by rp_init.
+void preload_xgpu_ws();
+void preload_xgpu();
+void preload_preduce();
+void preload_preduce_tma();
 int launch_fill_xi(float* dst, int64_t n, uint64_t seed, uint64_t w, uint64_t t, uint64_t j0,
                    void* stream, std::string* err);
 

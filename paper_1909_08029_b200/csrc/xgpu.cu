@@ -789,6 +789,13 @@ int dispatch(XTask& T, const XTask* d_tasks, int V, int max_parts, cudaStream_t 
 #undef RP_XL
 }
 
+template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
+void x_touch() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, xgpu_kernel<M, UA, UB, MOM, BF, KPM>);
+  cudaFuncGetAttributes(&a, xgpu_emul_kernel<M, UA, UB, MOM, BF, KPM>);
+}
+
 int check_task(const XTask& T, int* mmax, int* kpmax, bool* mom, std::string* err) {
   if (T.nparts < 1 || T.nparts > kMaxXParts) {
     *err = "xgpu: bad part count";
@@ -874,6 +881,19 @@ void xgpu_geometry(XPart& p, int64_t n) {
 int64_t xgpu_stage_region_bytes(int64_t n) {
   // kp rows of (S4 + 1) vectors, S4 <= n4/kp + tile: at most 4n + 16 * kp * (tile + 2)
   return 4 * n + 16LL * kMaxXGpus * (kTileF4 + 2);
+}
+
+void preload_xgpu() {  // every instantiation dispatch() can pick (see preload_xgpu_ws)
+#define RP_T(M, UA, UB, MOM, BF, KPM) x_touch<M, UA, UB, MOM, BF, KPM>()
+  RP_T(1, 4, 2, false, true, 2); RP_T(2, 2, 1, false, true, 2); RP_T(4, 1, 1, false, true, 2);
+  RP_T(8, 1, 1, false, true, 2); RP_T(1, 4, 1, false, true, 8); RP_T(2, 2, 1, false, true, 8);
+  RP_T(4, 1, 1, false, true, 8); RP_T(8, 1, 1, false, true, 8); RP_T(1, 2, 1, true, false, 8);
+  RP_T(2, 1, 1, true, false, 8); RP_T(4, 1, 1, true, false, 8); RP_T(8, 1, 1, true, false, 8);
+  RP_T(1, 4, 4, false, false, 2); RP_T(2, 2, 2, false, false, 2); RP_T(4, 1, 1, false, false, 2);
+  RP_T(8, 1, 1, false, false, 2); RP_T(1, 4, 1, false, false, 4); RP_T(2, 2, 1, false, false, 4);
+  RP_T(4, 1, 1, false, false, 4); RP_T(8, 1, 1, false, false, 4); RP_T(1, 4, 1, false, false, 8);
+  RP_T(2, 2, 1, false, false, 8); RP_T(4, 1, 1, false, false, 8); RP_T(8, 1, 1, false, false, 8);
+#undef RP_T
 }
 
 int launch_xgpu(XTask& T, void* stream, std::string* err) {

@@ -807,7 +807,28 @@ int launch_ws_m(XTask& T, const XTask* d_tasks, int V, int max_parts, cudaStream
   return RP_OK;
 }
 
+template <int M, int KPM, bool BF, int NOP, int S, int MINB>
+void ws_touch() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, xgpu_ws_kernel<M, KPM, BF, NOP, S, MINB>);
+  cudaFuncGetAttributes(&a, xgpu_ws_emul_kernel<M, KPM, BF, NOP, S, MINB>);
+}
+
 }  // namespace
+
+// Force-load every instantiation the dispatcher below can pick (CUDA lazy loading would load a
+// kernel at its first launch, inside a timed region: 10-11 ms stalls measured in round 2 when a
+// random schedule first produced a new (members, GPUs) combination).
+void preload_xgpu_ws() {
+#define RP_WS(M, KPM, BF, S, MINB) ws_touch<M, KPM, BF, 2 * M + KPM - 1, S, MINB>()
+  RP_WS(1, 2, true, 4, 2); RP_WS(1, 2, false, 4, 2); RP_WS(2, 2, true, 2, 2); RP_WS(2, 2, false, 2, 2);
+  RP_WS(4, 2, true, 2, 1); RP_WS(4, 2, false, 2, 1); RP_WS(8, 2, true, 1, 1); RP_WS(8, 2, false, 1, 1);
+  RP_WS(1, 4, true, 2, 2); RP_WS(1, 4, false, 2, 2); RP_WS(2, 4, true, 3, 1); RP_WS(2, 4, false, 3, 1);
+  RP_WS(4, 4, true, 2, 1); RP_WS(4, 4, false, 2, 1); RP_WS(8, 4, true, 1, 1); RP_WS(8, 4, false, 1, 1);
+  RP_WS(1, 8, true, 2, 1); RP_WS(1, 8, false, 2, 1); RP_WS(2, 8, true, 2, 1); RP_WS(2, 8, false, 2, 1);
+  RP_WS(8, 8, true, 1, 1); RP_WS(8, 8, false, 1, 1);
+#undef RP_WS
+}
 
 // Operand slots per stage: A needs 2M (x, g of every local member), B 2M + kp - 1 (+ the peers'
 // staged partials), C 1. Stages are sized so that two CTAs fit an SM where possible.
