@@ -123,7 +123,8 @@ struct XPart {
   int32_t slot;       // flag slot (lowest member of the group)
   int32_t rem;        // n mod 4
   uint64_t tag[kMaxXGpus];   // per peer: nonzero, unique per (group launch, GPU pair)
-  int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry)
+  int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry): CH = 1024-vector tiles per slice, nch chunks
+                             // per slice, chunk c = tiles [c CH / nch, (c+1) CH / nch) (balanced)
   float* x[kMaxXLocal];
   MemberUpdate u[kMaxXLocal];
   float* xfirst[kMaxXGpus];               // first local member replica of each group GPU (mapped)
@@ -168,7 +169,8 @@ struct XTask {
   unsigned long long watchdog_ns;          // flag-wait limit, 0 = wait forever
   XErr* err;                               // host-mapped error record (device address)
   int32_t nbuf;                            // shared-memory tile ring depth (launcher)
-  int32_t blag;                            // warp-specialized kernel: B runs blag (>= 2) iterations after A
+  int32_t blag;                            // warp-specialized kernel: B runs blag iterations after A
+  int32_t sig2;                            // ... with two flag-posting SIG jobs per iteration (blag >= 1)
   unsigned long long* cta_stat;            // profiling: per CTA ns [ring wait, signal wait, flag wait, total]
   int32_t nlocal;                          // fused intra-GPU groups (warp-specialized kernel only)
   XLocalGroup lg[kMaxXLocalGroups];

@@ -292,8 +292,9 @@ __device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(
 __device__ __forceinline__ ChunkRange chunk_range(const XPart& p, int o, int64_t c) {
   const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
   ChunkRange r;
-  r.lo = min(slo + c * p.CH, shi);
-  r.hi = min(slo + (c + 1) * p.CH, shi);
+  // balanced: chunk c = tiles [c CH / nch, (c+1) CH / nch) of the slice (CH = tiles per slice)
+  r.lo = min(slo + (c * p.CH) / p.nch * 1024, shi);
+  r.hi = min(slo + ((c + 1) * p.CH) / p.nch * 1024, shi);
   r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
   return r;
 }
@@ -852,8 +853,13 @@ int check_task(const XTask& T, int* mmax, int* kpmax, bool* mom, std::string* er
 
 // RP_XGPU_V2=1: the register (LDG/STG) version of this file for plain SGD too (comparison);
 // momentum steps always take it (their buffers are read and written per member)
+int sig2_setting() {  // RP_XGPU_SIG2: two SIG jobs per lane iteration in the warp-specialized kernel
+  static const int v = env_int("RP_XGPU_SIG2", 1) != 0;
+  return v;
+}
 int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stages (tuning)
-  static const int v = std::max(2, std::min(6, env_int("RP_XGPU_BLAG", 3)));  // 3: profiles/r02/sweep_blag_2gpu.txt
+  // one SIG per iteration: >= 2, 3 best (profiles/r02/sweep_blag_2gpu.txt); two SIGs: >= 1
+  static const int v = std::max(sig2_setting() ? 1 : 2, std::min(6, env_int("RP_XGPU_BLAG", sig2_setting() ? 1 : 3)));
   return v;
 }
 
@@ -867,15 +873,20 @@ void xgpu_geometry(XPart& p, int64_t n) {
   p.rem = static_cast<int32_t>(n - 4 * p.n4);
   p.S4 = ((p.n4 + p.kp - 1) / p.kp + kTileF4 - 1) / kTileF4 * kTileF4;
   p.S4 = std::max<int64_t>(p.S4, kTileF4);
-  // about kLaneIters pipeline iterations per lane, whole tiles of at least kMinTiles, at most
-  // kMaxChunks chunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job
-  // must see the same values: the geometry must agree across GPUs)
+  // every lane gets the same number of chunks (kLaneIters of them) and chunk sizes differ by at
+  // most one tile (a fixed chunk size left up to 28 % more work on some lanes than the average,
+  // and the slowest lane sets the kernel time); chunks of >= kMinTiles tiles on average, at most
+  // kMaxChunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job must see
+  // the same values: the geometry must agree across GPUs)
   static const int iters = std::max(1, env_int("RP_XGPU_ITERS", kLaneIters));
   static const int min_tiles = std::max(1, env_int("RP_XGPU_MIN_TILES", kMinTiles));
-  const int64_t ch = std::max<int64_t>((p.S4 + kXLanes * iters - 1) / (kXLanes * iters),
-                                       (p.S4 + kMaxChunks - 1) / kMaxChunks);
-  p.CH = std::max<int64_t>(kTileF4 * min_tiles, (ch + kTileF4 - 1) / kTileF4 * kTileF4);
-  p.nch = std::max<int64_t>(1, (p.S4 + p.CH - 1) / p.CH);
+  const int64_t tiles = p.S4 / kTileF4;
+  int64_t nch = static_cast<int64_t>(kXLanes) * iters;
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, tiles / min_tiles));
+  nch = std::min<int64_t>(nch, kMaxChunks);
+  if (nch > kXLanes) nch = nch / kXLanes * kXLanes;  // whole rounds of lanes
+  p.CH = tiles;
+  p.nch = std::max<int64_t>(1, nch);
 }
 
 int64_t xgpu_stage_region_bytes(int64_t n) {
@@ -902,6 +913,7 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   const int rc = check_task(T, &mmax, &kpmax, &mom, err);
   if (rc != RP_OK) return rc;
   T.blag = blag_setting();
+  T.sig2 = sig2_setting();
   if (!mom && !use_v2()) return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
   return dispatch<false>(T, nullptr, 1, T.nparts, static_cast<cudaStream_t>(stream), err, mmax, kpmax, mom);
 }
@@ -919,6 +931,7 @@ int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std:
   for (int v = 0; v < V; ++v) {
     tasks[v].nbuf = nbuf_setting();
     tasks[v].blag = blag_setting();
+    tasks[v].sig2 = sig2_setting();
   }
   const cudaError_t e = cudaMemcpyAsync(d_tasks, tasks, sizeof(XTask) * V, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) {

@@ -183,8 +183,9 @@ __device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(
 __device__ __forceinline__ Range chunk_range(const XPart& p, int o, int64_t c) {
   const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
   Range r;
-  r.lo = min(slo + c * p.CH, shi);
-  r.hi = min(slo + (c + 1) * p.CH, shi);
+  // balanced: chunk c = tiles [c CH / nch, (c+1) CH / nch) of the slice (CH = tiles per slice)
+  r.lo = min(slo + (c * p.CH) / p.nch * 1024, shi);
+  r.hi = min(slo + ((c + 1) * p.CH) / p.nch * 1024, shi);
   r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
   return r;
 }
@@ -621,7 +622,13 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         int64_t pA = -1, pB = -1;
         // B runs bl >= 2 iterations after A (A(c) flags are posted at the end of iteration c+1),
         // C runs 2 bl after A (B(c) flags at the end of iteration c+bl+1)
-        const int bl = T.blag, cl = 2 * T.blag;
+        // sig2 (default): two SIG jobs per iteration. The one after the A block posts the previous
+        // iteration's B flags (its B stores have completed once only the A block's are pending);
+        // the one at the end posts this iteration's A flags (only the B / C blocks' pending). A(c)
+        // flags then appear at the end of iteration c, so B(c) can run bl >= 1 iteration later,
+        // and B(c) flags after the next A block, so C(c) runs cl = bl + 1 iterations after A(c).
+        const bool sig2 = T.sig2 != 0;
+        const int bl = T.blag, cl = sig2 ? T.blag + 1 : 2 * T.blag;
         for (int64_t i = 0; ok && i < (iters ? iters + cl : 0); ++i) {
           const int64_t cA = i < iters ? ln + i * kXLanes : -1;
           const int64_t cB = (i >= bl && i - bl < iters) ? ln + (i - bl) * kXLanes : -1;
@@ -637,6 +644,10 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
               }
               if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJA, o, cA, stages, full, empty, jobs, P);
             }
+          if (ok && sig2) {
+            produce_marker<NOP, S>(kJSig, pi, -1, pB, sig++, full, empty, jobs, P);
+            pB = -1;
+          }
           if (ok && cB >= 0) {
             for (int d = 0; ok && d < p.kp; ++d)
               if (d != p.me)
@@ -656,11 +667,16 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
           if (ok) {
             emit_L(false);
             --iters_left;
-            produce_marker<NOP, S>(kJSig, pi, pA, pB, sig++, full, empty, jobs, P);
+            if (sig2)
+              produce_marker<NOP, S>(kJSig, pi, cA, -1, sig++, full, empty, jobs, P);
+            else
+              produce_marker<NOP, S>(kJSig, pi, pA, pB, sig++, full, empty, jobs, P);
           }
           pA = cA;
           pB = cB;
         }
+        if (ok && sig2 && pB >= 0)  // the last B block's flags
+          produce_marker<NOP, S>(kJSig, pi, -1, pB, sig++, full, empty, jobs, P);
       }
       if (ok) emit_L(true);  // leftovers (and every L tile of a CTA without lane work)
       if (!ok) *reinterpret_cast<volatile int*>(abort_w) = 1;
@@ -732,7 +748,12 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     if (lane == 0) bulk_wait_all();
-    if (T.cta_stat && warp == 0 && lane == 0) atomicAdd(T.cta_stat + 4 * blockIdx.x + 3, gtimer() - t_begin);
+    if (T.cta_stat && warp == 0 && lane == 0) {
+      const unsigned long long t_end = gtimer();
+      atomicAdd(T.cta_stat + 4 * blockIdx.x + 3, t_end - t_begin);
+      T.cta_stat[4 * 2048 + 2 * blockIdx.x] = t_begin;  // absolute begin / end of this CTA's work
+      T.cta_stat[4 * 2048 + 2 * blockIdx.x + 1] = t_end;
+    }
   }
 }
 
@@ -835,8 +856,8 @@ void preload_xgpu_ws() {
 int launch_xgpu_ws(XTask& T, const XTask* d_tasks, int V, int max_parts, void* stream, std::string* err, int mmax,
                    int kpmax, bool emu) {
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (T.blag < 2) {
-    *err = "xgpu_ws: blag < 2";
+  if (T.blag < (T.sig2 ? 1 : 2)) {
+    *err = "xgpu_ws: B lag below the flag protocol's minimum";
     return RP_EINVAL;
   }
 #define RP_WS(M, KPM, BF, S, MINB) \

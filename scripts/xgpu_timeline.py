@@ -17,7 +17,17 @@ def cta_breakdown(path):
     p = f"{base}.cta.{rank}"
     if not os.path.exists(p):
         return
-    a = np.fromfile(p, dtype=np.uint64).reshape(-1, 4).astype(np.float64)
+    raw = np.fromfile(p, dtype=np.uint64)
+    a = raw[:4 * 2048].reshape(-1, 4).astype(np.float64)
+    if raw.size >= 6 * 2048:   # absolute begin / end per CTA (warp-specialized kernel)
+        be = raw[4 * 2048:6 * 2048].reshape(-1, 2)
+        be = be[be[:, 1] > 0].astype(np.float64)
+        if len(be):
+            t0 = be[:, 0].min()
+            b, e = (be[:, 0] - t0) / 1e3, (be[:, 1] - t0) / 1e3
+            q = np.percentile(e, [0, 10, 50, 90, 100])
+            print(f"  CTA work begins within {b.max():.1f} us of the first; CTA end times (us after the first "
+                  f"begin) min/p10/p50/p90/max = " + "/".join(f"{v:.1f}" for v in q))
     a = a[a[:, 3] > 0]
     if not len(a):
         return
