@@ -195,6 +195,7 @@ struct rp_ctx {
   unsigned long long* vflags = nullptr;             // n_gpus flag arrays
   float* vstage = nullptr;                          // n_gpus * wpg staging regions
   rp::XTask* d_tasks = nullptr;                     // device copy of the emulated launch's tasks
+  unsigned int* claim = nullptr;                    // chunk-claim counters, kXClaimWords per (virtual) GPU
 };
 
 namespace {
@@ -507,6 +508,12 @@ int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<in
   T.bf16 = c->cfg.dtype == RP_DTYPE_BF16;
   T.watchdog_ns = c->watchdog_ns;
   T.err = c->xerr_dev;
+  static int dyn = -1;  // RP_XGPU_DYN=0: static chunk -> lane assignment (comparison)
+  if (dyn < 0) {
+    const char* v = std::getenv("RP_XGPU_DYN");
+    dyn = v && *v ? std::atoi(v) : 1;
+  }
+  T.claim = dyn && c->claim ? c->claim + static_cast<size_t>(c->emulate ? gpu : 0) * rp::kXClaimWords : nullptr;
   const int64_t esz = T.bf16 ? 2 : 4;  // bytes per replica element
   int64_t nvl = 0, hbm = 0;
   for (int64_t q : seqs) {
@@ -1009,6 +1016,11 @@ int rp_init(const rp_config* cfg, rp_ctx** out) {
       }
       std::memset(c->xerr, 0, sizeof(rp::XErr));
       const int nflag = c->emulate ? k.n_gpus : 1;
+      if ((e = cudaMalloc(&c->claim, sizeof(unsigned int) * rp::kXClaimWords * nflag)) != cudaSuccess ||
+          (e = cudaMemset(c->claim, 0, sizeof(unsigned int) * rp::kXClaimWords * nflag)) != cudaSuccess) {
+        rp_finalize(c);
+        return cuda_fail(e, "rp_init: claim counters");
+      }
       if ((e = cudaMalloc(&c->flags, rp::kFlagWords * 8 * nflag)) != cudaSuccess ||
           (e = cudaMemset(c->flags, 0, rp::kFlagWords * 8 * nflag)) != cudaSuccess ||
           (e = cudaMalloc(&c->stage, c->stage_region * wpg * nflag)) != cudaSuccess) {
@@ -1183,6 +1195,7 @@ int rp_finalize(rp_ctx* c) {
     if (c->flags) cudaFree(c->flags);
     if (c->stage) cudaFree(c->stage);
     if (c->d_tasks) cudaFree(c->d_tasks);
+    if (c->claim) cudaFree(c->claim);
     if (c->xerr) cudaFreeHost(c->xerr);
     if (c->prof) {
       // dump the item timeline of the last cross-GPU launch

@@ -171,6 +171,8 @@ struct XTask {
   int32_t nbuf;                            // shared-memory tile ring depth (launcher)
   int32_t blag;                            // warp-specialized kernel: B runs blag iterations after A
   int32_t sig2;                            // ... with two flag-posting SIG jobs per iteration (blag >= 1)
+  unsigned int* claim;                     // dynamic chunk claiming: [2 part][L tiles, done CTAs], zeroed
+                                           // between launches by the kernel (nullptr = static lanes)
   unsigned long long* cta_stat;            // profiling: per CTA ns [ring wait, signal wait, flag wait, total]
   int32_t nlocal;                          // fused intra-GPU groups (warp-specialized kernel only)
   XLocalGroup lg[kMaxXLocalGroups];
@@ -179,6 +181,7 @@ struct XTask {
 
 // Lanes of the cross-GPU kernel (chunk c runs on lane c mod kXLanes on every GPU).
 constexpr int kXLanes = 296;
+constexpr int kXClaimWords = 2 * kMaxXParts + 2;  // per (virtual) GPU
 // Slice and chunk geometry of a part (kp set) for n elements (depends on n and kp only).
 void xgpu_geometry(XPart& p, int64_t n);
 // Bytes of one staging region (one cross-GPU group owned by one local worker).

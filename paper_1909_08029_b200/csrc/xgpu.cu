@@ -914,7 +914,10 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   if (rc != RP_OK) return rc;
   T.blag = blag_setting();
   T.sig2 = sig2_setting();
-  if (!mom && !use_v2()) return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
+  if (!mom && !use_v2()) {
+    if (T.claim && !T.sig2) T.claim = nullptr;  // dynamic claiming runs the two-SIG pipeline
+    return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
+  }
   return dispatch<false>(T, nullptr, 1, T.nparts, static_cast<cudaStream_t>(stream), err, mmax, kpmax, mom);
 }
 
@@ -932,6 +935,7 @@ int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std:
     tasks[v].nbuf = nbuf_setting();
     tasks[v].blag = blag_setting();
     tasks[v].sig2 = sig2_setting();
+    if (tasks[v].claim && (!tasks[v].sig2 || mom || use_v2())) tasks[v].claim = nullptr;
   }
   const cudaError_t e = cudaMemcpyAsync(d_tasks, tasks, sizeof(XTask) * V, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) {

@@ -615,7 +615,113 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         int64_t want = all || iters_left <= 0 ? left : (left + iters_left - 1) / iters_left;
         for (; want > 0 && lq < ltiles; --want, lq += ncta) produce_L<BF, NOP, S>(T, lq, stages, full, empty, jobs, P);
       };
-      for (int idx = cta; ok && idx < total; idx += ncta) {
+      // ---- one lane iteration's A / B / C blocks (part + chunk each, -1 = none) ----
+      auto block_A = [&](int pi, int64_t c) {
+        const XPart& p = T.part[pi];
+        for (int j = 1; ok && j < p.kp; ++j) {
+          const int o = (p.me + j) % p.kp;  // spread the pushes over the owners
+          const unsigned long long bit = 1ull << (8 * pi + o);
+          if (!(ready_seen & bit)) {
+            ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[o], kFlagReady, 0), p.tag[o], p.slot, p.gpu[o],
+                           kFlagReady, 0);
+            ready_seen |= bit;
+          }
+          if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJA, o, c, stages, full, empty, jobs, P);
+        }
+      };
+      auto block_B = [&](int pi, int64_t c) {
+        const XPart& p = T.part[pi];
+        for (int d = 0; ok && d < p.kp; ++d)
+          if (d != p.me)
+            ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, c), p.tag[d], p.slot, p.gpu[d], kFlagA, c);
+        fence_async_all();  // the peers' partials (acquired) are read next by the async proxy
+        if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJB, p.me, c, stages, full, empty, jobs, P);
+      };
+      auto block_C = [&](int pi, int64_t c) {
+        const XPart& p = T.part[pi];
+        for (int j = 1; ok && j < p.kp; ++j) {
+          const int o = (p.me + j) % p.kp;
+          ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[o], kFlagB, c), p.tag[o], p.slot, p.gpu[o], kFlagB, c);
+          fence_async_all();
+          if (ok && p.m > 1) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJC, o, c, stages, full, empty, jobs, P);
+        }
+      };
+      if (T.claim) {
+        // ---- dynamic chunk claiming (default) ----
+        // Chunks are claimed from one counter per part (parts in ascending seq, chunks ascending),
+        // so a CTA that runs faster takes more chunks and the kernel has no static tail (the
+        // slowest of 296 statically assigned lanes set the kernel time: CTA end times spread
+        // 25 % at ResNet-50 size, profiles/r02/). Iteration i: A(claim i), SIG posting B flags of
+        // iteration i-1, B(claim i - bl), C(claim i - cl), SIG posting A flags of iteration i.
+        // Claims are monotone per GPU in (part, chunk), and a chunk's A flags depend only on B
+        // waits of smaller claims, so no cycle of waits can form across GPUs.
+        constexpr int kRing = 8;
+        int cpi[kRing];
+        int64_t cch[kRing];
+        const int bl = T.blag, cl = T.blag + 1;
+        int cur = 0;                   // part being claimed from
+        int64_t nclaim = 0;            // claims made by this CTA
+        int64_t last = -1;             // iteration of the last successful claim
+        int64_t nch_all = 0;
+        for (int pi = 0; pi < T.nparts; ++pi) nch_all += T.part[pi].nch;
+        const int64_t lper = ltiles > 0 ? (ltiles + max(nch_all, static_cast<int64_t>(1)) - 1) / max(nch_all, static_cast<int64_t>(1)) : 0;
+        unsigned int* const lctr = T.claim + 2 * kMaxXParts;
+        int piB_prev = -1;
+        int64_t cB_prev = -1;
+        for (int64_t i = 0; ok; ++i) {
+          int piA = -1;
+          int64_t cA = -1;
+          while (cur < T.nparts) {  // claim the next chunk (part order, then chunk order)
+            const int64_t c = static_cast<int64_t>(atomicAdd(T.claim + 2 * cur, 1u));
+            if (c < T.part[cur].nch) {
+              piA = cur;
+              cA = c;
+              break;
+            }
+            ++cur;
+          }
+          if (cA >= 0) {
+            cpi[i % kRing] = piA;
+            cch[i % kRing] = cA;
+            last = i;
+            ++nclaim;
+          } else if (last < 0 || i > last + cl) {
+            break;
+          }
+          // claims happen in iterations 0 .. last (consecutive, until the counters run out)
+          const bool hasB = i - bl >= 0 && i - bl <= last;
+          const int piB = hasB ? cpi[(i - bl) % kRing] : -1;
+          const int64_t cB = hasB ? cch[(i - bl) % kRing] : -1;
+          const bool hasC = i >= cl && i - cl <= last;
+          if (cA >= 0) block_A(piA, cA);
+          if (ok && piB_prev >= 0) {
+            produce_marker<NOP, S>(kJSig, piB_prev, -1, cB_prev, sig++, full, empty, jobs, P);
+            piB_prev = -1;
+          }
+          if (ok && hasB) block_B(piB, cB);
+          if (ok && hasC) block_C(cpi[(i - cl) % kRing], cch[(i - cl) % kRing]);
+          if (ok) {
+            for (int64_t q = 0; q < lper; ++q) {  // fused intra-GPU tiles, claimed as they come
+              const int64_t t = static_cast<int64_t>(atomicAdd(lctr, 1u));
+              if (t >= ltiles) break;
+              produce_L<BF, NOP, S>(T, t, stages, full, empty, jobs, P);
+            }
+            if (cA >= 0) produce_marker<NOP, S>(kJSig, piA, cA, -1, sig++, full, empty, jobs, P);
+          }
+          if (hasB) {
+            piB_prev = piB;
+            cB_prev = cB;
+          }
+        }
+        if (ok && piB_prev >= 0) produce_marker<NOP, S>(kJSig, piB_prev, -1, cB_prev, sig++, full, empty, jobs, P);
+        while (ok) {  // leftover fused tiles
+          const int64_t t = static_cast<int64_t>(atomicAdd(lctr, 1u));
+          if (t >= ltiles) break;
+          produce_L<BF, NOP, S>(T, t, stages, full, empty, jobs, P);
+        }
+        (void)nclaim;
+      }
+      for (int idx = cta; ok && !T.claim && idx < total; idx += ncta) {
         const int pi = idx % T.nparts, ln = idx / T.nparts;
         const XPart& p = T.part[pi];
         const int64_t iters = ln < p.nch ? (p.nch - 1 - ln) / kXLanes + 1 : 0;
@@ -678,9 +784,17 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         if (ok && sig2 && pB >= 0)  // the last B block's flags
           produce_marker<NOP, S>(kJSig, pi, -1, pB, sig++, full, empty, jobs, P);
       }
-      if (ok) emit_L(true);  // leftovers (and every L tile of a CTA without lane work)
+      if (ok && !T.claim) emit_L(true);  // leftovers (and every L tile of a CTA without lane work)
       if (!ok) *reinterpret_cast<volatile int*>(abort_w) = 1;
       produce_marker<NOP, S>(kJEnd, 0, -1, -1, 0, full, empty, jobs, P);
+      if (T.claim) {  // the last CTA done claiming resets the counters for the next launch
+        __threadfence();
+        if (atomicAdd(T.claim + 2 * kMaxXParts + 1, 1u) == static_cast<unsigned>(ncta) - 1) {
+          for (int q = 0; q < 2 * kMaxXParts + 1; ++q) T.claim[q] = 0;
+          __threadfence();
+          T.claim[2 * kMaxXParts + 1] = 0;
+        }
+      }
     }
     __syncwarp();
   } else {  // ---------------- consumers ----------------
