@@ -65,7 +65,7 @@ constexpr int kTileRows = 4;
 constexpr int64_t kTileF4 = kRowF4 * kTileRows;   // 1024 vectors: a 16 KB fp32 tile
 constexpr int kNbufDefault = 3;                   // shared-memory tile ring (48 KB; RP_XGPU_NBUF 2..8)
 constexpr int kNbufMax = 8;
-constexpr int kLaneIters = 3;                     // target pipeline iterations per lane
+constexpr int kLaneIters = 3;                     // (unused default; see xgpu_geometry)
 constexpr int kMinTiles = 2;                      // smallest chunk: 2 tiles (32 KB fp32)
 
 __device__ __forceinline__ float4 ldv(const float* p) {
@@ -878,9 +878,15 @@ void xgpu_geometry(XPart& p, int64_t n) {
   // and the slowest lane sets the kernel time); chunks of >= kMinTiles tiles on average, at most
   // kMaxChunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job must see
   // the same values: the geometry must agree across GPUs)
-  static const int iters = std::max(1, env_int("RP_XGPU_ITERS", kLaneIters));
+  // Default: about 8 tiles (128 KB) per chunk, 2..6 chunks per lane -- ResNet-50 slices take 2-3
+  // chunks per lane, VGG-16 slices 5-6 (6 gave +7 % at VGG size, 3 was best at ResNet-50 size:
+  // profiles/r02/sweep_dyn_2gpu.txt).
+  static const int iters_env = env_int("RP_XGPU_ITERS", 0);
   static const int min_tiles = std::max(1, env_int("RP_XGPU_MIN_TILES", kMinTiles));
   const int64_t tiles = p.S4 / kTileF4;
+  const int iters = iters_env > 0 ? iters_env
+                                  : static_cast<int>(std::max<int64_t>(
+                                        2, std::min<int64_t>(6, (tiles + kXLanes * 4) / (kXLanes * 8))));
   int64_t nch = static_cast<int64_t>(kXLanes) * iters;
   nch = std::min<int64_t>(nch, std::max<int64_t>(1, tiles / min_tiles));
   nch = std::min<int64_t>(nch, kMaxChunks);

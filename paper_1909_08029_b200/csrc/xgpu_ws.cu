@@ -706,7 +706,9 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
               if (t >= ltiles) break;
               produce_L<BF, NOP, S>(T, t, stages, full, empty, jobs, P);
             }
-            if (cA >= 0) produce_marker<NOP, S>(kJSig, piA, cA, -1, sig++, full, empty, jobs, P);
+            // always delimit the iteration (even without an A block): the next SIG_a's wait for
+            // "only the groups since the last SIG pending" must not cover this iteration's B stores
+            produce_marker<NOP, S>(kJSig, cA >= 0 ? piA : 0, cA, -1, sig++, full, empty, jobs, P);
           }
           if (hasB) {
             piB_prev = piB;
