@@ -878,15 +878,15 @@ void xgpu_geometry(XPart& p, int64_t n) {
   // and the slowest lane sets the kernel time); chunks of >= kMinTiles tiles on average, at most
   // kMaxChunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job must see
   // the same values: the geometry must agree across GPUs)
-  // Default: about 8 tiles (128 KB) per chunk, 2..6 chunks per lane -- ResNet-50 slices take 2-3
-  // chunks per lane, VGG-16 slices 5-6 (6 gave +7 % at VGG size, 3 was best at ResNet-50 size:
-  // profiles/r02/sweep_dyn_2gpu.txt).
+  // Default: about 4 tiles (64 KB) per chunk, 3..6 chunks per lane -- ResNet-50 slices take 3
+  // chunks per lane, VGG-16 slices 6 (6 gave +7 % at VGG size, 3 was best at ResNet-50 size and
+  // 2 lost 12 % on the 8-worker problem at N = 4: profiles/r02/sweep_dyn_2gpu.txt, r02/final_4gpu/).
   static const int iters_env = env_int("RP_XGPU_ITERS", 0);
   static const int min_tiles = std::max(1, env_int("RP_XGPU_MIN_TILES", kMinTiles));
   const int64_t tiles = p.S4 / kTileF4;
   const int iters = iters_env > 0 ? iters_env
                                   : static_cast<int>(std::max<int64_t>(
-                                        2, std::min<int64_t>(6, (tiles + kXLanes * 4) / (kXLanes * 8))));
+                                        3, std::min<int64_t>(6, (tiles + kXLanes * 3) / (kXLanes * 4))));
   int64_t nch = static_cast<int64_t>(kXLanes) * iters;
   nch = std::min<int64_t>(nch, std::max<int64_t>(1, tiles / min_tiles));
   nch = std::min<int64_t>(nch, kMaxChunks);
