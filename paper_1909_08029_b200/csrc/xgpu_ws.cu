@@ -648,22 +648,25 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
       };
       if (T.claim) {
         // ---- dynamic chunk claiming (default) ----
-        // Chunks are claimed from one counter per part (parts in ascending seq, chunks ascending),
+        // Chunks are claimed from one counter (chunk-major over the parts, parts in ascending seq),
         // so a CTA that runs faster takes more chunks and the kernel has no static tail (the
         // slowest of 296 statically assigned lanes set the kernel time: CTA end times spread
         // 25 % at ResNet-50 size, profiles/r02/). Iteration i: A(claim i), SIG posting B flags of
         // iteration i-1, B(claim i - bl), C(claim i - cl), SIG posting A flags of iteration i.
-        // Claims are monotone per GPU in (part, chunk), and a chunk's A flags depend only on B
-        // waits of smaller claims, so no cycle of waits can form across GPUs.
+        // Claims are monotone per GPU in (chunk, group seq), one order shared by all GPUs, and a
+        // chunk's A flags depend only on B waits of smaller claims, so no cycle of waits can form.
         constexpr int kRing = 8;
         int cpi[kRing];
         int64_t cch[kRing];
         const int bl = T.blag, cl = T.blag + 1;
-        int cur = 0;                   // part being claimed from
+        int cur = 0;                   // 1 once the claim counter ran out
         int64_t nclaim = 0;            // claims made by this CTA
         int64_t last = -1;             // iteration of the last successful claim
-        int64_t nch_all = 0;
-        for (int pi = 0; pi < T.nparts; ++pi) nch_all += T.part[pi].nch;
+        int64_t nch_all = 0, max_nch = 0;
+        for (int pi = 0; pi < T.nparts; ++pi) {
+          nch_all += T.part[pi].nch;
+          max_nch = max(max_nch, T.part[pi].nch);
+        }
         const int64_t lper = ltiles > 0 ? (ltiles + max(nch_all, static_cast<int64_t>(1)) - 1) / max(nch_all, static_cast<int64_t>(1)) : 0;
         unsigned int* const lctr = T.claim + 2 * kMaxXParts;
         int piB_prev = -1;
@@ -671,14 +674,23 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         for (int64_t i = 0; ok; ++i) {
           int piA = -1;
           int64_t cA = -1;
-          while (cur < T.nparts) {  // claim the next chunk (part order, then chunk order)
-            const int64_t c = static_cast<int64_t>(atomicAdd(T.claim + 2 * cur, 1u));
-            if (c < T.part[cur].nch) {
-              piA = cur;
+          // claim the next (chunk, part) pair in chunk-major order (parts ascending seq): all of
+          // a GPU's groups advance together, as their peers expect (part-major claiming ran a
+          // GPU's groups one after another and chained the GPUs' steps: -14 % on the 8-worker
+          // problem at N = 4, profiles/r02/); the order is the same on every GPU of a group
+          while (cur == 0) {
+            const int64_t q = static_cast<int64_t>(atomicAdd(T.claim, 1u));
+            const int64_t c = q / T.nparts;
+            const int pq = static_cast<int>(q - c * T.nparts);
+            if (c >= max_nch) {
+              cur = 1;  // exhausted
+              break;
+            }
+            if (c < T.part[pq].nch) {
+              piA = pq;
               cA = c;
               break;
             }
-            ++cur;
           }
           if (cA >= 0) {
             cpi[i % kRing] = piA;
