@@ -514,6 +514,16 @@ int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<in
     dyn = v && *v ? std::atoi(v) : 1;
   }
   T.claim = dyn && c->claim ? c->claim + static_cast<size_t>(c->emulate ? gpu : 0) * rp::kXClaimWords : nullptr;
+  // claim order (xgpu_ws.cu): part by part when every group of the launch comes from a static
+  // schedule (seq < 0), chunk-major for Group-Generator groups; RP_XGPU_CLAIM=part|chunk overrides
+  static int order = -1;
+  if (order < 0) {
+    const char* v = std::getenv("RP_XGPU_CLAIM");
+    order = !v || !*v ? 2 : (std::string(v) == "part" ? 1 : 0);
+  }
+  bool all_static = true;
+  for (int64_t q : seqs) all_static = all_static && q < 0;
+  T.part_major = order == 2 ? (all_static ? 1 : 0) : order;
   const int64_t esz = T.bf16 ? 2 : 4;  // bytes per replica element
   int64_t nvl = 0, hbm = 0;
   for (int64_t q : seqs) {

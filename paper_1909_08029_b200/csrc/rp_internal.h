@@ -171,7 +171,9 @@ struct XTask {
   int32_t nbuf;                            // shared-memory tile ring depth (launcher)
   int32_t blag;                            // warp-specialized kernel: B runs blag iterations after A
   int32_t sig2;                            // ... with two flag-posting SIG jobs per iteration (blag >= 1)
-  unsigned int* claim;                     // dynamic chunk claiming: [2 part][L tiles, done CTAs], zeroed
+  int32_t part_major;                      // claim order: 1 = part by part, 0 = chunk-major over parts
+  unsigned int* claim;                     // dynamic chunk claiming: [chunk-major, part 0..7, ...,
+                                           // [L tiles, done CTAs] (kXClaimWords words), zeroed
                                            // between launches by the kernel (nullptr = static lanes)
   unsigned long long* cta_stat;            // profiling: per CTA ns [ring wait, signal wait, flag wait, total]
   int32_t nlocal;                          // fused intra-GPU groups (warp-specialized kernel only)
@@ -181,7 +183,7 @@ struct XTask {
 
 // Lanes of the cross-GPU kernel (chunk c runs on lane c mod kXLanes on every GPU).
 constexpr int kXLanes = 296;
-constexpr int kXClaimWords = 2 * kMaxXParts + 2;  // per (virtual) GPU
+constexpr int kXClaimWords = 2 * kMaxXParts + 2;  // per (virtual) GPU; the L / done words at 2 kMaxXParts
 // Slice and chunk geometry of a part (kp set) for n elements (depends on n and kp only).
 void xgpu_geometry(XPart& p, int64_t n);
 // Bytes of one staging region (one cross-GPU group owned by one local worker).

@@ -674,11 +674,25 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         for (int64_t i = 0; ok; ++i) {
           int piA = -1;
           int64_t cA = -1;
-          // claim the next (chunk, part) pair in chunk-major order (parts ascending seq): all of
-          // a GPU's groups advance together, as their peers expect (part-major claiming ran a
-          // GPU's groups one after another and chained the GPUs' steps: -14 % on the 8-worker
-          // problem at N = 4, profiles/r02/); the order is the same on every GPU of a group
-          while (cur == 0) {
+          // Claim order (the same on every GPU of a group, so no cycle of waits can form):
+          // chunk-major (default for Group-Generator steps): every (chunk, part) pair in chunk
+          // order, parts ascending seq -- all of a GPU's groups advance together; part-major
+          // claiming ran them one after another and chained the GPUs' random groups (-14 % on the
+          // 8-worker problem at N = 4). Part-major (static schedules): a GPU in two groups
+          // finishes the first early, so that group's peers start their next step while it works
+          // on the second -- the fixed schedule turns the skew into overlap across steps
+          // (configs[3] layout at N = 4: 5,474 part-major vs 4,430 chunk-major worker-steps/s).
+          // profiles/r02/claim_order_4gpu.txt
+          while (T.part_major && cur < T.nparts) {  // part-major: a GPU's groups one after another
+            const int64_t c = static_cast<int64_t>(atomicAdd(T.claim + 1 + cur, 1u));
+            if (c < T.part[cur].nch) {
+              piA = cur;
+              cA = c;
+              break;
+            }
+            ++cur;
+          }
+          while (!T.part_major && cur == 0) {
             const int64_t q = static_cast<int64_t>(atomicAdd(T.claim, 1u));
             const int64_t c = q / T.nparts;
             const int pq = static_cast<int>(q - c * T.nparts);
