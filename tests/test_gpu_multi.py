@@ -184,3 +184,11 @@ def test_multi_gpu_native_executor(gpus, spec):
     if _ngpu() < gpus:
         pytest.skip(f"needs {gpus} GPUs")
     _run(gpus, {"sample": 0, "rule": None, "native": True, **spec})
+
+
+def test_multi_gpu_watchdog_reports_timeout():
+    # a peer that never arrives: the flag wait gives up after watchdog_s, the kernel ends, the
+    # host call returns RP_ETIMEOUT and the CUDA context stays usable (no __trap)
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, {}, script="multi_gpu_watchdog_worker.py", timeout=300)
