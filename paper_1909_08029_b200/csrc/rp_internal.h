@@ -123,8 +123,10 @@ struct XPart {
   int32_t slot;       // flag slot (lowest member of the group)
   int32_t rem;        // n mod 4
   uint64_t tag[kMaxXGpus];   // per peer: nonzero, unique per (group launch, GPU pair)
-  int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry): CH = 1024-vector tiles per slice, nch chunks
-                             // per slice, chunk c = tiles [c CH / nch, (c+1) CH / nch) (balanced)
+  int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry): nch chunks per slice; chunks c < nch - nsmall
+                             // split CH 1024-vector tiles evenly (balanced), the last nsmall chunks
+                             // are one tile each (tiles CH + (c - nch + nsmall))
+  int64_t nsmall;
   float* x[kMaxXLocal];
   MemberUpdate u[kMaxXLocal];
   float* xfirst[kMaxXGpus];               // first local member replica of each group GPU (mapped)

@@ -292,9 +292,12 @@ __device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(
 __device__ __forceinline__ ChunkRange chunk_range(const XPart& p, int o, int64_t c) {
   const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
   ChunkRange r;
-  // balanced: chunk c = tiles [c CH / nch, (c+1) CH / nch) of the slice (CH = tiles per slice)
-  r.lo = min(slo + (c * p.CH) / p.nch * 1024, shi);
-  r.hi = min(slo + ((c + 1) * p.CH) / p.nch * 1024, shi);
+  // balanced big chunks: tiles [c CH / nbig, (c+1) CH / nbig); then nsmall one-tile chunks
+  const int64_t nbig = p.nch - p.nsmall;
+  const int64_t t_lo = c < nbig ? (c * p.CH) / nbig : p.CH + (c - nbig);
+  const int64_t t_hi = c < nbig ? ((c + 1) * p.CH) / nbig : t_lo + 1;
+  r.lo = min(slo + t_lo * 1024, shi);
+  r.hi = min(slo + t_hi * 1024, shi);
   r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
   return r;
 }
@@ -636,7 +639,8 @@ __device__ __forceinline__ void xgpu_body(const XTask& T, int cta, int ncta) {
 }
 
 template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
-__global__ void __launch_bounds__(kXThreads, RP_XGPU_MINB) xgpu_kernel(const __grid_constant__ XTask T) {
+__global__ void __launch_bounds__(kXThreads, (M >= 4 || MOM) ? 1 : RP_XGPU_MINB)
+    xgpu_kernel(const __grid_constant__ XTask T) {
   xgpu_body<M, UA, UB, MOM, BF, KPM>(T, blockIdx.x, gridDim.x);
 }
 
@@ -644,7 +648,8 @@ __global__ void __launch_bounds__(kXThreads, RP_XGPU_MINB) xgpu_kernel(const __g
 // virtual GPU v on CTAs v, v + V, v + 2V, ... (all co-resident: a spinning CTA never starves the
 // CTA it waits for; separate spinning launches on one GPU are not guaranteed to run together).
 template <int M, int UA, int UB, bool MOM, bool BF, int KPM>
-__global__ void __launch_bounds__(kXThreads, RP_XGPU_MINB) xgpu_emul_kernel(const XTask* __restrict__ tasks, int V) {
+__global__ void __launch_bounds__(kXThreads, (M >= 4 || MOM) ? 1 : RP_XGPU_MINB)
+    xgpu_emul_kernel(const XTask* __restrict__ tasks, int V) {
   const int v = blockIdx.x % V;
   xgpu_body<M, UA, UB, MOM, BF, KPM>(tasks[v], blockIdx.x / V, gridDim.x / V);
 }
@@ -772,8 +777,8 @@ int dispatch(XTask& T, const XTask* d_tasks, int V, int max_parts, cudaStream_t 
     RP_XL(8, 1, 1, true, false, 8);
   }
   if (kpmax <= 2 && !EMU) {
-    if (mmax <= 1) RP_XL(1, 4, 4, false, false, 2);
-    if (mmax <= 2) RP_XL(2, 2, 2, false, false, 2);
+    if (mmax <= 1) RP_XL(1, 4, 2, false, false, 2);
+    if (mmax <= 2) RP_XL(2, 2, 1, false, false, 2);
     if (mmax <= 4) RP_XL(4, 1, 1, false, false, 2);
     RP_XL(8, 1, 1, false, false, 2);
   }
@@ -887,12 +892,20 @@ void xgpu_geometry(XPart& p, int64_t n) {
   const int iters = iters_env > 0 ? iters_env
                                   : static_cast<int>(std::max<int64_t>(
                                         3, std::min<int64_t>(6, (tiles + kXLanes * 3) / (kXLanes * 4))));
+  // RP_XGPU_TAIL = t > 0 (experiment, off): the last t chunks are single tiles, taken last under
+  // dynamic claiming to shorten the kernel's tail. Measured slower (ResNet-50 xall 0.62 vs 0.67 of
+  // 770 GB/s at t = 296: the per-chunk flag and SIG overhead outweighs the shorter tail,
+  // profiles/r02/sweep_tail_2gpu.txt), so 0.
+  static const int tail_env = env_int("RP_XGPU_TAIL", 0);
+  const int64_t nsmall = std::min<int64_t>(std::max(0, tail_env), tiles / 4);
+  const int64_t tb = tiles - nsmall;
   int64_t nch = static_cast<int64_t>(kXLanes) * iters;
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, tiles / min_tiles));
-  nch = std::min<int64_t>(nch, kMaxChunks);
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, tb / min_tiles));
+  nch = std::min<int64_t>(nch, kMaxChunks - nsmall);
   if (nch > kXLanes) nch = nch / kXLanes * kXLanes;  // whole rounds of lanes
-  p.CH = tiles;
-  p.nch = std::max<int64_t>(1, nch);
+  p.CH = tb;
+  p.nsmall = nsmall;
+  p.nch = std::max<int64_t>(1, nch) + nsmall;
 }
 
 int64_t xgpu_stage_region_bytes(int64_t n) {
@@ -906,7 +919,7 @@ void preload_xgpu() {  // every instantiation dispatch() can pick (see preload_x
   RP_T(8, 1, 1, false, true, 2); RP_T(1, 4, 1, false, true, 8); RP_T(2, 2, 1, false, true, 8);
   RP_T(4, 1, 1, false, true, 8); RP_T(8, 1, 1, false, true, 8); RP_T(1, 2, 1, true, false, 8);
   RP_T(2, 1, 1, true, false, 8); RP_T(4, 1, 1, true, false, 8); RP_T(8, 1, 1, true, false, 8);
-  RP_T(1, 4, 4, false, false, 2); RP_T(2, 2, 2, false, false, 2); RP_T(4, 1, 1, false, false, 2);
+  RP_T(1, 4, 2, false, false, 2); RP_T(2, 2, 1, false, false, 2); RP_T(4, 1, 1, false, false, 2);
   RP_T(8, 1, 1, false, false, 2); RP_T(1, 4, 1, false, false, 4); RP_T(2, 2, 1, false, false, 4);
   RP_T(4, 1, 1, false, false, 4); RP_T(8, 1, 1, false, false, 4); RP_T(1, 4, 1, false, false, 8);
   RP_T(2, 2, 1, false, false, 8); RP_T(4, 1, 1, false, false, 8); RP_T(8, 1, 1, false, false, 8);

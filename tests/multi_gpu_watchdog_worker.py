@@ -21,9 +21,9 @@ def main():
     torch.cuda.set_device(rank)
     n = 100_003
     ctx = Context(2, n, n_gpus=2, rank=rank, device=rank, group_size=2, watchdog_s=2)
-    X = torch.zeros(2 * n + 64, device="cuda")
-    x = X[:n]
-    g = X[n + 32:2 * n + 32]
+    ld = (n + 63) // 64 * 64                 # 256-byte aligned rows, like the runner
+    X = torch.zeros((2, ld), device="cuda")
+    x, g = X[0, :n], X[1, :n]
     ctx.bind_worker(rank, x, g)
     ctx.peer_setup(None)
     ok = True
