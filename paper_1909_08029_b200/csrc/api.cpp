@@ -590,6 +590,27 @@ int build_task(rp_ctx* c, const std::vector<int64_t>& seqs, const std::vector<in
 // This GPU's parts of every cross-GPU group of the batch, in ONE xgpu launch (caller holds mu;
 // members' arrival events already joined into `stream`). Emulated GPUs: every virtual GPU's
 // parts in ONE cooperative launch.
+// RP_DEBUG_POISON=1 (race check; compute-sanitizer is closed on this pool): before a cross
+// launch, fill the staging rows this GPU owns with 0xFF bytes (a NaN pattern). The peers may push
+// into them only after this launch posts READY, so a B stage that read a partial before it
+// arrived would fold a NaN into the mean and fail the bit-exact parity tests.
+int poison_staging(const rp::XTask& T, cudaStream_t stream) {
+  for (int pi = 0; pi < T.nparts; ++pi) {
+    const rp::XPart& p = T.part[pi];
+    const size_t bytes = static_cast<size_t>(p.kp) * static_cast<size_t>(p.S4 + 1) * 16;
+    CUDA_TRY(cudaMemsetAsync(p.stage[p.me], 0xFF, bytes, stream));
+  }
+  return RP_OK;
+}
+bool poison_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RP_DEBUG_POISON");
+    v = e && *e && std::atoi(e) != 0;
+  }
+  return v == 1;
+}
+
 int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t stream, int max_ctas,
                  const std::vector<int64_t>& local) {
   if (!c->peers_ready) return fail(RP_ESTATE, "cross-GPU group before rp_peer_import");
@@ -617,6 +638,11 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
       nvl += a;
       hbm += b;
     }
+    if (poison_enabled())
+      for (int d = 0; d < V; ++d) {
+        const int prc = poison_staging(tasks[d], stream);
+        if (prc != RP_OK) return prc;
+      }
     const int rc = rp::launch_xgpu_emulated(tasks.data(), V, c->d_tasks, stream, &err);
     if (rc != RP_OK) return fail(rc, err);
   } else {
@@ -640,6 +666,10 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
         if (c->cta_stat) cudaMemsetAsync(c->cta_stat, 0, sizeof(unsigned long long) * 6 * 2048, stream);
         T.cta_stat = c->cta_stat;
       }
+    }
+    if (poison_enabled()) {
+      rc = poison_staging(T, stream);
+      if (rc != RP_OK) return rc;
     }
     rc = rp::launch_xgpu(T, stream, &err);
     if (rc != RP_OK) return fail(rc, err);

@@ -160,3 +160,20 @@ def test_emulated_non_finite_gradients(dtype):
         assert nan[17] and nan[4001]
         assert np.array_equal(got[~nan].view(np.uint32), X[w][~nan].view(np.uint32)), w
     r.close()
+
+
+def test_emulated_suite_with_poisoned_staging():
+    # race check without compute-sanitizer (closed on this pool): RP_DEBUG_POISON=1 fills every
+    # owner's staging rows with a NaN pattern before each cross launch; a B stage that read a
+    # peer's partial before its flag would fold NaN into the mean -> bit-exact parity fails
+    import os
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_emulated.py"), "-q",
+                        "-m", "gpu", "-x", "-p", "no:cacheprovider", "-k", "not poisoned and not full_r50"],
+                       capture_output=True, text=True, cwd=root, timeout=900,
+                       env={**os.environ, "RP_DEBUG_POISON": "1"})
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]

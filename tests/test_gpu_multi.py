@@ -147,6 +147,19 @@ def test_multi_gpu_geometry_knobs(gpus, env, spec):
     _run(gpus, {"sample": 0, "rule": None, **spec}, env=env)
 
 
+@pytest.mark.parametrize("gpus,spec", [
+    # RP_DEBUG_POISON: owners' staging rows NaN-filled before every cross launch (race check)
+    (2, dict(wpg=4, n=300_007, k=3, mode="gd", steps=12)),
+    (2, dict(wpg=2, n=200_003, k=3, mode="static", rule="shift_k", steps=10, dtype="bf16")),
+    (4, dict(wpg=1, n=500_009, k=3, mode="gd", steps=12)),
+    (4, dict(wpg=2, n=300_007, k=3, mode="static", rule="shift_k", steps=9, momentum=[0.9, 1e-4])),
+])
+def test_multi_gpu_poisoned_staging(gpus, spec):
+    if _ngpu() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    _run(gpus, {"sample": 0, "rule": None, **spec}, env={"RP_DEBUG_POISON": "1"})
+
+
 BF16_CASES = [
     # bf16 replicas across GPUs (reading R26): fp32 partials over NVLink, the mean rounded once
     # to bf16 and pushed as bf16; bit-exact vs the oracle's fused_group_update_bf16
