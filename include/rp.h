@@ -30,7 +30,15 @@
  *     manner").
  *   - Worker placement (reading R6): worker w lives on GPU w / workers_per_gpu.
  *     One process drives one GPU (rank = GPU index); that process binds and
- *     drives exactly the workers of its GPU.
+ *     drives exactly the workers of its GPU (RP_FLAG_EMULATE: every virtual
+ *     GPU's workers, one device).
+ *   - One device model per process: kernel attributes, occupancy and the SM
+ *     count are cached per process at first use, and the intra-GPU kernel's
+ *     tile-counter ring is per device; a process may hold several contexts, on
+ *     one or several identical B200s, but not on GPUs of different kinds.
+ *   - rp_init loads every kernel instantiation of the library up front (CUDA
+ *     lazy loading would otherwise load a kernel at its first launch, which a
+ *     random schedule may first reach inside a timed region).
  */
 #ifndef RP_H
 #define RP_H
