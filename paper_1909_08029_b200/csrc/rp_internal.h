@@ -174,6 +174,8 @@ struct XTask {
   int32_t blag;                            // warp-specialized kernel: B runs blag iterations after A
   int32_t sig2;                            // ... with two flag-posting SIG jobs per iteration (blag >= 1)
   int32_t part_major;                      // claim order: 1 = part by part, 0 = chunk-major over parts
+  int32_t lookahead;                       // dynamic claiming: claim + push the next A block while a
+                                           // B block's flags are not yet posted (RP_XGPU_LOOKAHEAD)
   unsigned int* claim;                     // dynamic chunk claiming: [chunk-major, part 0..7, ...,
                                            // [L tiles, done CTAs] (kXClaimWords words), zeroed
                                            // between launches by the kernel (nullptr = static lanes)

@@ -868,6 +868,16 @@ int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stag
   return v;
 }
 
+// RP_XGPU_LOOKAHEAD = 1 (experiment, off): under dynamic claiming, when a B block's A flags are not
+// all posted, the producer claims and pushes the next chunk's A block first. Parity holds (emulated
+// and 2/4-GPU suites) but it is slower everywhere (ResNet-50 xall at N = 2: 0.61 vs 0.68 of 770 GB/s;
+// configs[3] layout at N = 4: 5,140 vs 5,435 worker-steps/s): the B block a peer waits for is pushed
+// later, profiles/r02/sweep_lookahead_{2,4}gpu.txt. So 0.
+int lookahead_setting() {
+  static const int v = env_int("RP_XGPU_LOOKAHEAD", 0) != 0;
+  return v;
+}
+
 bool use_v2() {
   static const int v = env_int("RP_XGPU_V2", 0);
   return v == 1;
@@ -933,6 +943,7 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   if (rc != RP_OK) return rc;
   T.blag = blag_setting();
   T.sig2 = sig2_setting();
+  T.lookahead = lookahead_setting();
   if (!mom && !use_v2()) {
     if (T.claim && !T.sig2) T.claim = nullptr;  // dynamic claiming runs the two-SIG pipeline
     return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
@@ -954,6 +965,7 @@ int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std:
     tasks[v].nbuf = nbuf_setting();
     tasks[v].blag = blag_setting();
     tasks[v].sig2 = sig2_setting();
+    tasks[v].lookahead = lookahead_setting();
     if (tasks[v].claim && (!tasks[v].sig2 || mom || use_v2())) tasks[v].claim = nullptr;
   }
   const cudaError_t e = cudaMemcpyAsync(d_tasks, tasks, sizeof(XTask) * V, cudaMemcpyHostToDevice, s);

@@ -674,9 +674,9 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
         unsigned int* const lctr = T.claim + 2 * kMaxXParts;
         int piB_prev = -1;
         int64_t cB_prev = -1;
-        for (int64_t i = 0; ok; ++i) {
-          int piA = -1;
-          int64_t cA = -1;
+        int pre_pi = -1;               // lookahead: a claim whose A block is already pushed
+        int64_t pre_c = -1;
+        auto claim_next = [&](int& piA, int64_t& cA) {
           // Claim order (the same on every GPU of a group, so no cycle of waits can form):
           // chunk-major (default for Group-Generator steps): every (chunk, part) pair in chunk
           // order, parts ascending seq -- all of a GPU's groups advance together; part-major
@@ -709,6 +709,26 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
               break;
             }
           }
+        };
+        // all peers' A flags of (pi, c) posted (non-blocking probe)
+        auto a_posted = [&](int pi, int64_t c) {
+          const XPart& p = T.part[pi];
+          for (int d = 0; d < p.kp; ++d)
+            if (d != p.me && ld_acquire_sys(flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, c)) != p.tag[d]) return false;
+          return true;
+        };
+        for (int64_t i = 0; ok; ++i) {
+          int piA = -1;
+          int64_t cA = -1;
+          bool a_done = false;
+          if (pre_c >= 0) {
+            piA = pre_pi;
+            cA = pre_c;
+            pre_c = -1;
+            a_done = true;
+          } else {
+            claim_next(piA, cA);
+          }
           if (cA >= 0) {
             cpi[i % kRing] = piA;
             cch[i % kRing] = cA;
@@ -722,12 +742,24 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
           const int piB = hasB ? cpi[(i - bl) % kRing] : -1;
           const int64_t cB = hasB ? cch[(i - bl) % kRing] : -1;
           const bool hasC = i >= cl && i - cl <= last;
-          if (cA >= 0) block_A(piA, cA);
+          if (cA >= 0 && !a_done) block_A(piA, cA);
           if (ok && piB_prev >= 0) {
             produce_marker<NOP, S>(kJSig, piB_prev, -1, cB_prev, sig++, full, empty, jobs, P);
             piB_prev = -1;
           }
-          if (ok && hasB) block_B(piB, cB);
+          // an A block pushed ahead (last iteration, before its B block) is complete once the
+          // SIG above has drained (nothing was committed since the last SIG): post its flags now
+          if (ok && a_done) produce_marker<NOP, S>(kJSig, piA, cA, -1, sig++, full, empty, jobs, P);
+          if (ok && hasB) {
+            // lookahead: the B block's partials are not all in yet -- push the next claim's A
+            // block first (it waits for nothing), then block on the flags. Claims stay monotone,
+            // and the pushed-ahead A flags are posted at the next iteration's first SIG.
+            if (T.lookahead && (T.part_major ? cur < T.nparts : cur == 0) && !a_posted(piB, cB)) {
+              claim_next(pre_pi, pre_c);
+              if (pre_c >= 0) block_A(pre_pi, pre_c);
+            }
+            if (ok) block_B(piB, cB);
+          }
           if (ok && hasC) block_C(cpi[(i - cl) % kRing], cch[(i - cl) % kRing]);
           if (ok) {
             for (int64_t q = 0; q < lper; ++q) {  // fused intra-GPU tiles, claimed as they come
@@ -737,7 +769,7 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
             }
             // always delimit the iteration (even without an A block): the next SIG_a's wait for
             // "only the groups since the last SIG pending" must not cover this iteration's B stores
-            produce_marker<NOP, S>(kJSig, cA >= 0 ? piA : 0, cA, -1, sig++, full, empty, jobs, P);
+            produce_marker<NOP, S>(kJSig, cA >= 0 ? piA : 0, a_done ? -1 : cA, -1, sig++, full, empty, jobs, P);
           }
           if (hasB) {
             piB_prev = piB;
