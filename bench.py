@@ -353,11 +353,13 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
         if gpm:
             gpm.start()
         ev0.record(s0)
+        h0 = time.perf_counter()
         if args.per_call:
             for _ in range(steps):
                 runner.step()
         else:
             runner.run_native(steps)
+        host_ms = (time.perf_counter() - h0) * 1e3      # host enqueue time of the K steps (no sync)
         ev1.record(s0)
         runner.synchronize()
         g = gpm.stop() if gpm else None
@@ -368,7 +370,7 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
     ms = D.max(ev0.elapsed_time(ev1))
     recs = runner.ctx.timing_records()
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    per_rank = D.gather({"recs": recs, "launches": launches, "clocks": clk.summary(), "gpm": g,
+    per_rank = D.gather({"recs": recs, "launches": launches, "clocks": clk.summary(), "gpm": g, "host_ms": host_ms,
                          "hbm": st1["bytes_hbm"] - st0["bytes_hbm"], "nvl": st1["bytes_nvlink"] - st0["bytes_nvlink"],
                          "cross": st1["cross_gpu_groups"] - st0["cross_gpu_groups"]})
     if os.environ.get("RP_BENCH_DUMP_RECS") and rank == 0:   # debugging: every rank's per-launch records
@@ -425,6 +427,7 @@ def run_ours(args, wl, name, D, steps=None, warmup=None, e2e=True, delay_us=None
         "roofline": roof,
         "gpu_launches": sum(r["launches"] for r in per_rank),
         "clocks": merge_clocks([r["clocks"] for r in per_rank]),
+        "host_enqueue_ms": [round(r["host_ms"], 2) for r in per_rank],   # per rank, K steps, no sync
         "e2e": e2e_line,
     }
 
@@ -931,6 +934,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N>1: skip the cfg4 / NCCL-group / cfg5 extras")
     ap.add_argument("--extra-steps", type=int, default=30)
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="diagnostics only: skip the e2e measurement (the line then has no e2e number)")
     ap.add_argument("--per-call", action="store_true",
                     help="drive each lockstep step from Python through the per-call API instead of rp_lockstep_run")
     ap.add_argument("--slow", type=float, default=2.0, help="cfg5: extra delay of worker 0 in units of T_c")
@@ -941,10 +946,14 @@ def main():
     ap.add_argument("--k", type=int, default=0, help="cfg5: group size override (2 + --gg random = AD-PSGD)")
     ap.add_argument("--delay", choices=["host", "device"], default="host",
                     help="cfg5: synthetic compute as a host sleep (P:1395) or a device busy wait")
+    ap.add_argument("--size", type=int, default=0,
+                    help="diagnostics only: override the workload's parameter count (the line names it)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     wl = WORKLOADS[args.workload]
+    if args.size > 0:
+        wl = dict(wl, n=args.size, desc=wl["desc"] + f" [diagnostic size override: n = {args.size}]")
     if args.impl == "reference":
         line = run_reference(args, wl, args.workload)
         if line:
@@ -966,7 +975,7 @@ def main():
         if wl.get("delayed"):
             def dl(w):
                 return args.tc_us * (1 + args.slow) if w == 0 else args.tc_us
-        line = run_ours(args, wl, args.workload, D, delay_us=dl)
+        line = run_ours(args, wl, args.workload, D, delay_us=dl, e2e=not args.no_e2e)
         if D.n == 1 and line is not None and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(wl, D.n, budget_s=args.cpu_budget)
         if D.n > 1 and args.workload == "r50x8" and not args.no_extras:

@@ -662,8 +662,8 @@ int launch_cross(rp_ctx* c, const std::vector<int64_t>& seqs_in, cudaStream_t st
       c->prof_items = items;
       if (c->prof) {
         cudaMemsetAsync(c->prof, 0, items * sizeof(rp::XItemRecord), stream);
-        if (!c->cta_stat) cudaMalloc(&c->cta_stat, sizeof(unsigned long long) * 6 * 2048);
-        if (c->cta_stat) cudaMemsetAsync(c->cta_stat, 0, sizeof(unsigned long long) * 6 * 2048, stream);
+        if (!c->cta_stat) cudaMalloc(&c->cta_stat, sizeof(unsigned long long) * rp::kCtaStatWords);
+        if (c->cta_stat) cudaMemsetAsync(c->cta_stat, 0, sizeof(unsigned long long) * rp::kCtaStatWords, stream);
         T.cta_stat = c->cta_stat;
       }
     }
@@ -1250,7 +1250,7 @@ int rp_finalize(rp_ctx* c) {
       cudaFree(c->prof);
     }
     if (c->cta_stat) {  // per-CTA breakdown [ring wait, signal wait, flag wait, total] ns of the last launch
-      std::vector<unsigned long long> h(6 * 2048);
+      std::vector<unsigned long long> h(rp::kCtaStatWords);
       if (cudaMemcpy(h.data(), c->cta_stat, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
         const std::string path = c->prof_path + ".cta." + std::to_string(c->cfg.rank);
         if (FILE* f = std::fopen(path.c_str(), "wb")) {

@@ -174,6 +174,8 @@ struct XTask {
   int32_t blag;                            // warp-specialized kernel: B runs blag iterations after A
   int32_t sig2;                            // ... with two flag-posting SIG jobs per iteration (blag >= 1)
   int32_t part_major;                      // claim order: 1 = part by part, 0 = chunk-major over parts
+  int32_t early_a;                         // dynamic claiming: A flags posted after the B block's first
+                                           // tile, not at the iteration's end (RP_XGPU_EARLY_A)
   int32_t lookahead;                       // dynamic claiming: claim + push the next A block while a
                                            // B block's flags are not yet posted (RP_XGPU_LOOKAHEAD)
   unsigned int* claim;                     // dynamic chunk claiming: [chunk-major, part 0..7, ...,
@@ -187,6 +189,12 @@ struct XTask {
 
 // Lanes of the cross-GPU kernel (chunk c runs on lane c mod kXLanes on every GPU).
 constexpr int kXLanes = 296;
+// RP_XGPU_PROFILE per-CTA records (u64 words, 2048 CTAs): [0, 4*2048) ns [ring wait, signal wait,
+// flag wait, total]; [4*2048, 6*2048) absolute begin / end; then kCtaSig SIG times per CTA (time | 1:
+// posts A flags | 2: posts B flags), kCtaWait flag waits per CTA as (start | kind, end), 2 counters
+constexpr int kCtaSig = 32, kCtaWait = 32;
+constexpr int64_t kCtaSigBase = 6 * 2048, kCtaWaitBase = kCtaSigBase + 2048 * kCtaSig,
+                  kCtaCntBase = kCtaWaitBase + 2048 * 2 * kCtaWait, kCtaStatWords = kCtaCntBase + 2048 * 2;
 constexpr int kXClaimWords = 2 * kMaxXParts + 2;  // per (virtual) GPU; the L / done words at 2 kMaxXParts
 // Slice and chunk geometry of a part (kp set) for n elements (depends on n and kp only).
 void xgpu_geometry(XPart& p, int64_t n);

@@ -873,6 +873,17 @@ int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stag
 // and 2/4-GPU suites) but it is slower everywhere (ResNet-50 xall at N = 2: 0.61 vs 0.68 of 770 GB/s;
 // configs[3] layout at N = 4: 5,140 vs 5,435 worker-steps/s): the B block a peer waits for is pushed
 // later, profiles/r02/sweep_lookahead_{2,4}gpu.txt. So 0.
+// RP_XGPU_EARLY_A (default 1): under dynamic claiming a chunk's A flags are posted from a SIG after the
+// first tile of the iteration's B block instead of at the iteration's end, so the peers' B blocks of
+// that chunk wait less (per-iteration timelines: B blocks waited for A flags posted behind a whole B
+// block, profiles/r02/timeline_sig_*.txt). Measured (profiles/r02/sweep_early_a_{2,4}gpu.txt, two runs
+// each): N = 4 configs[3] layout 5,439 / 5,374 -> 5,587 / 5,581, xall +5-9 %, cfg3 +1 %, r50x8 -0.5 %
+// (noise); N = 2 xall / cfg3 +3 %, r50x8 and configs[3] layout unchanged.
+int early_a_setting() {
+  static const int v = env_int("RP_XGPU_EARLY_A", 1) != 0;
+  return v;
+}
+
 int lookahead_setting() {
   static const int v = env_int("RP_XGPU_LOOKAHEAD", 0) != 0;
   return v;
@@ -944,6 +955,7 @@ int launch_xgpu(XTask& T, void* stream, std::string* err) {
   T.blag = blag_setting();
   T.sig2 = sig2_setting();
   T.lookahead = lookahead_setting();
+  T.early_a = early_a_setting();
   if (!mom && !use_v2()) {
     if (T.claim && !T.sig2) T.claim = nullptr;  // dynamic claiming runs the two-SIG pipeline
     return launch_xgpu_ws(T, nullptr, 1, T.nparts, stream, err, mmax, kpmax, false);
@@ -966,6 +978,7 @@ int launch_xgpu_emulated(XTask* tasks, int V, XTask* d_tasks, void* stream, std:
     tasks[v].blag = blag_setting();
     tasks[v].sig2 = sig2_setting();
     tasks[v].lookahead = lookahead_setting();
+    tasks[v].early_a = early_a_setting();
     if (tasks[v].claim && (!tasks[v].sig2 || mom || use_v2())) tasks[v].claim = nullptr;
   }
   const cudaError_t e = cudaMemcpyAsync(d_tasks, tasks, sizeof(XTask) * V, cudaMemcpyHostToDevice, s);

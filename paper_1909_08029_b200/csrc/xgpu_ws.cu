@@ -171,7 +171,16 @@ __device__ __forceinline__ bool wait_flag(const XTask& T, const unsigned long lo
   if (ld_acquire_sys(f) == tag) return true;
   const unsigned long long t0 = T.cta_stat ? gtimer() : 0;
   const bool ok = wait_flag_slow(T, f, tag, slot, src, kind, c);
-  if (T.cta_stat) atomicAdd(T.cta_stat + 4 * blockIdx.x + 2, gtimer() - t0);
+  if (T.cta_stat) {
+    const unsigned long long t1 = gtimer();
+    atomicAdd(T.cta_stat + 4 * blockIdx.x + 2, t1 - t0);
+    const unsigned long long q = T.cta_stat[kCtaCntBase + 2 * blockIdx.x + 1]++;  // producer lane only
+    if (q < kCtaWait) {
+      unsigned long long* r = T.cta_stat + kCtaWaitBase + (2 * kCtaWait) * blockIdx.x + 2 * q;
+      r[0] = (t0 & ~3ull) | static_cast<unsigned>(kind & 3);
+      r[1] = t1;
+    }
+  }
   return ok;
 }
 
@@ -465,10 +474,29 @@ __device__ __forceinline__ void advance(Prod& P) {
   }
 }
 
+template <int NOP, int S>
+__device__ __forceinline__ void produce_marker(int kind, int pi, int64_t pA, int64_t pB, int sig, uint64_t* full,
+                                               uint64_t* empty, Job* jobs, Prod& P) {
+  const int s = acquire_stage<NOP, S>(P, empty);
+  Job& J = jobs[s];
+  J.kind = kind;
+  J.pi = pi;
+  J.cnt = 0;
+  J.pA = pA;
+  J.pB = pB;
+  J.sig = sig;
+  J.tail = 0;
+  mbar_arrive(&full[s]);
+  advance<S>(P);
+}
+
 template <int M, int KPM, bool BF, int NOP, int S>
 __device__ void produce_tiles(const XTask& T, int pi, int kind, int o, int64_t c, float4* stages, uint64_t* full,
-                              uint64_t* empty, Job* jobs, Prod& P) {
+                              uint64_t* empty, Job* jobs, Prod& P, int mk_pi = -1, int64_t mk_pA = -1,
+                              int* sig = nullptr) {
+  // mk_pA >= 0: a SIG job posting the A flags of (mk_pi, mk_pA) goes in after the first tile
   const XPart& p = T.part[pi];
+  bool marked = mk_pA < 0;
   const Range r = chunk_range(p, kind == kJB ? p.me : o, c);
   const bool need_tail = r.tail && (kind != kJC || p.m > 1);
   for (int64_t t0 = r.lo; t0 < r.hi || (t0 == r.lo && need_tail); t0 += kT) {
@@ -513,8 +541,13 @@ __device__ void produce_tiles(const XTask& T, int pi, int kind, int o, int64_t c
       }
     }
     advance<S>(P);
+    if (!marked) {
+      produce_marker<NOP, S>(kJSig, mk_pi, mk_pA, -1, (*sig)++, full, empty, jobs, P);
+      marked = true;
+    }
     if (r.hi <= r.lo) break;  // tail-only job
   }
+  if (!marked) produce_marker<NOP, S>(kJSig, mk_pi, mk_pA, -1, (*sig)++, full, empty, jobs, P);
 }
 
 // L tile q of this launch (group q mod nlocal, tile q / nlocal): x and g of every member
@@ -553,21 +586,6 @@ __device__ void produce_L(const XTask& T, int64_t q, float4* stages, uint64_t* f
   advance<S>(P);
 }
 
-template <int NOP, int S>
-__device__ __forceinline__ void produce_marker(int kind, int pi, int64_t pA, int64_t pB, int sig, uint64_t* full,
-                                               uint64_t* empty, Job* jobs, Prod& P) {
-  const int s = acquire_stage<NOP, S>(P, empty);
-  Job& J = jobs[s];
-  J.kind = kind;
-  J.pi = pi;
-  J.cnt = 0;
-  J.pA = pA;
-  J.pB = pB;
-  J.sig = sig;
-  J.tail = 0;
-  mbar_arrive(&full[s]);
-  advance<S>(P);
-}
 
 template <int M, int KPM, bool BF, int NOP, int S>
 __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) {
@@ -632,13 +650,13 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
           if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJA, o, c, stages, full, empty, jobs, P);
         }
       };
-      auto block_B = [&](int pi, int64_t c) {
+      auto block_B = [&](int pi, int64_t c, int mk_pi = -1, int64_t mk_pA = -1) {
         const XPart& p = T.part[pi];
         for (int d = 0; ok && d < p.kp; ++d)
           if (d != p.me)
             ok = wait_flag(T, flag_at(T.my_flags, p.slot, p.gpu[d], kFlagA, c), p.tag[d], p.slot, p.gpu[d], kFlagA, c);
         fence_async_all();  // the peers' partials (acquired) are read next by the async proxy
-        if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJB, p.me, c, stages, full, empty, jobs, P);
+        if (ok) produce_tiles<M, KPM, BF, NOP, S>(T, pi, kJB, p.me, c, stages, full, empty, jobs, P, mk_pi, mk_pA, &sig);
       };
       auto block_C = [&](int pi, int64_t c) {
         const XPart& p = T.part[pi];
@@ -743,13 +761,21 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
           const int64_t cB = hasB ? cch[(i - bl) % kRing] : -1;
           const bool hasC = i >= cl && i - cl <= last;
           if (cA >= 0 && !a_done) block_A(piA, cA);
+          bool sig_a_emitted = false;
           if (ok && piB_prev >= 0) {
             produce_marker<NOP, S>(kJSig, piB_prev, -1, cB_prev, sig++, full, empty, jobs, P);
             piB_prev = -1;
+            sig_a_emitted = true;
           }
           // an A block pushed ahead (last iteration, before its B block) is complete once the
           // SIG above has drained (nothing was committed since the last SIG): post its flags now
           if (ok && a_done) produce_marker<NOP, S>(kJSig, piA, cA, -1, sig++, full, empty, jobs, P);
+          // early A flags (T.early_a): post this iteration's A flags from a SIG after the first tile of
+          // the B block instead of at the iteration's end -- its wait (everything before the SIG above
+          // completed) covers the A block, and the peers' B blocks of this claim can start a B block
+          // earlier. Needs a SIG between the A block and that one: an empty one if none was posted.
+          const bool early = T.early_a && hasB && cA >= 0 && !a_done;
+          if (ok && early && !sig_a_emitted) produce_marker<NOP, S>(kJSig, 0, -1, -1, sig++, full, empty, jobs, P);
           if (ok && hasB) {
             // lookahead: the B block's partials are not all in yet -- push the next claim's A
             // block first (it waits for nothing), then block on the flags. Claims stay monotone,
@@ -758,7 +784,10 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
               claim_next(pre_pi, pre_c);
               if (pre_c >= 0) block_A(pre_pi, pre_c);
             }
-            if (ok) block_B(piB, cB);
+            if (ok) {
+              if (early) block_B(piB, cB, piA, cA);
+              else block_B(piB, cB);
+            }
           }
           if (ok && hasC) block_C(cpi[(i - cl) % kRing], cch[(i - cl) % kRing]);
           if (ok) {
@@ -769,7 +798,7 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
             }
             // always delimit the iteration (even without an A block): the next SIG_a's wait for
             // "only the groups since the last SIG pending" must not cover this iteration's B stores
-            produce_marker<NOP, S>(kJSig, cA >= 0 ? piA : 0, a_done ? -1 : cA, -1, sig++, full, empty, jobs, P);
+            produce_marker<NOP, S>(kJSig, cA >= 0 ? piA : 0, a_done || early ? -1 : cA, -1, sig++, full, empty, jobs, P);
           }
           if (hasB) {
             piB_prev = piB;
@@ -876,7 +905,14 @@ __device__ __forceinline__ void xgpu_ws_body(const XTask& T, int cta, int ncta) 
           mbar_arrive(&empty[s]);
           unsigned long long t1 = T.cta_stat && warp == 0 ? gtimer() : 0;
           bulk_wait_pending(ncommit);  // this warp's groups of the previous iteration have completed
-          if (T.cta_stat && warp == 0) atomicAdd(T.cta_stat + 4 * blockIdx.x + 1, gtimer() - t1);
+          if (T.cta_stat && warp == 0) {
+            const unsigned long long t2 = gtimer();
+            atomicAdd(T.cta_stat + 4 * blockIdx.x + 1, t2 - t1);
+            const unsigned long long q = T.cta_stat[kCtaCntBase + 2 * blockIdx.x]++;
+            if (q < kCtaSig)
+              T.cta_stat[kCtaSigBase + kCtaSig * blockIdx.x + q] =
+                  (t2 & ~3ull) | (J.pA >= 0 ? 1u : 0u) | (J.pB >= 0 ? 2u : 0u);
+          }
           ncommit = 0;
           fence_async_all();
           int* cnt = &sigcnt[J.sig % kSigRing];

@@ -39,9 +39,70 @@ def cta_breakdown(path):
           f"[2] the producer's flag waits)")
 
 
+def sig_timeline(path, bin_us=10.0):
+    """Per-iteration view (warp-specialized kernel): SIG times and producer flag waits over the kernel."""
+    import os
+    base, rank = path.rsplit(".", 1)
+    p = f"{base}.cta.{rank}"
+    if not os.path.exists(p):
+        return
+    raw = np.fromfile(p, dtype=np.uint64)
+    SIG, WAIT = 32, 32
+    sb = 6 * 2048
+    wb = sb + 2048 * SIG
+    cb = wb + 2048 * 2 * WAIT
+    if raw.size < cb + 2 * 2048:
+        return
+    be = raw[4 * 2048:6 * 2048].reshape(-1, 2)
+    live = np.nonzero(be[:, 1] > 0)[0]
+    if not len(live):
+        return
+    t0 = be[live, 0].min()
+    span = (be[live, 1].max() - t0) / 1e3
+    print(f"  [{rank}] kernel: first CTA begin at globaltimer {int(t0)} ns, last CTA end +{span:.1f} us")
+    cnt = raw[cb:cb + 2 * 2048].reshape(-1, 2)
+    sig = raw[sb:wb].reshape(2048, SIG)
+    rows = []
+    for c in live:
+        ns = int(min(cnt[c, 0], SIG))
+        rows.append([((int(v) & ~3) - int(t0)) / 1e3 for v in sig[c, :ns]])
+    kmax = max(len(r) for r in rows)
+    line = []
+    for k in range(kmax):
+        v = np.array([r[k] for r in rows if len(r) > k])
+        line.append(f"{k}:{np.percentile(v, 50):.0f}({len(v)})")
+    print("  SIG k: median us after kernel begin (CTAs reaching it): " + " ".join(line))
+    wt = raw[wb:cb].reshape(2048, WAIT, 2)
+    nb = int(span // bin_us) + 1
+    busy = {0: np.zeros(nb), 1: np.zeros(nb), 2: np.zeros(nb)}
+    tot = {0: 0.0, 1: 0.0, 2: 0.0}
+    for c in live:
+        nw = int(min(cnt[c, 1], WAIT))
+        for q in range(nw):
+            k = int(wt[c, q, 0]) & 3
+            a = ((int(wt[c, q, 0]) & ~3) - int(t0)) / 1e3
+            b = (int(wt[c, q, 1]) - int(t0)) / 1e3
+            tot[k] += b - a
+            i = int(a // bin_us)
+            while a < b and i < nb:
+                e = min(b, (i + 1) * bin_us)
+                busy[k][i] += e - a
+                a, i = e, i + 1
+    names = {0: "A-flag", 1: "B-flag", 2: "READY"}
+    n = len(live)
+    for k in (2, 0, 1):
+        if tot[k] > 0:
+            prof = " ".join(f"{x / (n * bin_us):.2f}" for x in busy[k])
+            print(f"  {names[k]} waits: {tot[k] / n:.1f} us per CTA; fraction of CTAs waiting per {bin_us:.0f} us bin: {prof}")
+    ends = np.sort((be[live, 1] - t0) / 1e3)
+    act = " ".join(f"{(ends > (i + 1) * bin_us).mean():.2f}" for i in range(nb))
+    print(f"  fraction of CTAs still running at the end of each bin: {act}")
+
+
 def main():
     for path in sys.argv[1:]:
         cta_breakdown(path)
+        sig_timeline(path)
         rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 4)
         rec = rec[rec[:, 0] > 0]
         if not len(rec):  # the warp-specialized kernel records only the per-CTA breakdown
