@@ -16,11 +16,14 @@
 // peer's first member for B, to the other local members for C), then release the stage on its
 // `empty` mbarrier. Loads, arithmetic and NVLink pushes of different tiles overlap.
 //
-// Flags (deferred, as in xgpu.cu): a SIG job ends every lane iteration; each consumer warp
-// waits until only its bulk groups of this iteration are pending (so its groups of the
-// previous iteration have completed), makes them visible to the generic proxy and arrives on a
-// shared counter with acq_rel; the last warp releases at system scope and posts the previous
-// iteration's A and B flags. A wait for a peer's flag (producer warp) past the watchdog limit
+// Flags (deferred): flags are posted by SIG jobs in the stage stream. At a SIG each consumer
+// warp waits until only its bulk groups committed since the previous SIG are pending (so
+// everything before the previous SIG has completed), makes them visible to the generic proxy and
+// arrives on a shared counter with acq_rel; the last warp releases at system scope and posts the
+// flags the SIG carries. Default (dynamic chunk claiming), iteration i of a CTA: A(claim i),
+// SIG_a (B flags of iteration i-1), B(claim i-1) with SIG_m after its first tile (A flags of
+// claim i), C(claim i-2), fused intra-GPU tiles, SIG_b (delimiter). The static-lane fallback keeps
+// xgpu.cu's lane pipeline. A wait for a peer's flag (producer warp) past the watchdog limit
 // records it in host-mapped memory and ends the CTA's work (an END job lets the consumers out).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
