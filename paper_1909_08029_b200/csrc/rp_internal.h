@@ -125,8 +125,8 @@ struct XPart {
   uint64_t tag[kMaxXGpus];   // per peer: nonzero, unique per (group launch, GPU pair)
   int64_t n4, S4, CH, nch;   // geometry (xgpu_geometry): nch chunks per slice; chunks c < nch - nsmall
                              // split CH 1024-vector tiles evenly (balanced), the last nsmall chunks
-                             // are one tile each (tiles CH + (c - nch + nsmall))
-  int64_t nsmall;
+                             // are tail_w tiles each (tiles CH + (c - nch + nsmall) * tail_w, ...)
+  int32_t nsmall, tail_w;
   float* x[kMaxXLocal];
   MemberUpdate u[kMaxXLocal];
   float* xfirst[kMaxXGpus];               // first local member replica of each group GPU (mapped)

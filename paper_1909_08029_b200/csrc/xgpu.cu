@@ -292,10 +292,10 @@ __device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(
 __device__ __forceinline__ ChunkRange chunk_range(const XPart& p, int o, int64_t c) {
   const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
   ChunkRange r;
-  // balanced big chunks: tiles [c CH / nbig, (c+1) CH / nbig); then nsmall one-tile chunks
+  // balanced big chunks: tiles [c CH / nbig, (c+1) CH / nbig); then nsmall chunks of tail_w tiles
   const int64_t nbig = p.nch - p.nsmall;
-  const int64_t t_lo = c < nbig ? (c * p.CH) / nbig : p.CH + (c - nbig);
-  const int64_t t_hi = c < nbig ? ((c + 1) * p.CH) / nbig : t_lo + 1;
+  const int64_t t_lo = c < nbig ? (c * p.CH) / nbig : p.CH + (c - nbig) * p.tail_w;
+  const int64_t t_hi = c < nbig ? ((c + 1) * p.CH) / nbig : t_lo + p.tail_w;
   r.lo = min(slo + t_lo * 1024, shi);
   r.hi = min(slo + t_hi * 1024, shi);
   r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
@@ -913,19 +913,27 @@ void xgpu_geometry(XPart& p, int64_t n) {
   const int iters = iters_env > 0 ? iters_env
                                   : static_cast<int>(std::max<int64_t>(
                                         3, std::min<int64_t>(6, (tiles + kXLanes * 3) / (kXLanes * 4))));
-  // RP_XGPU_TAIL = t > 0 (experiment, off): the last t chunks are single tiles, taken last under
-  // dynamic claiming to shorten the kernel's tail. Measured slower (ResNet-50 xall 0.62 vs 0.67 of
-  // 770 GB/s at t = 296: the per-chunk flag and SIG overhead outweighs the shorter tail,
-  // profiles/r02/sweep_tail_2gpu.txt), so 0.
+  // RP_XGPU_TAIL = t > 0 (experiment, off): the last t chunks are RP_XGPU_TAIL_TILES tiles each
+  // (default 1), taken last under dynamic claiming to shorten the kernel's tail; RP_XGPU_TAIL_KEEP=1
+  // takes them out of the big chunks' count (same number of chunks, so the same flag overhead).
+  // t = 296 single tiles on top of the big chunks measured slower (ResNet-50 xall 0.62 vs 0.67 of
+  // 770 GB/s: the per-chunk flag and SIG overhead outweighs the shorter tail,
+  // profiles/r02/sweep_tail_2gpu.txt); carved out of the big chunks (KEEP=1) at N = 4: 296 x 2 tiles
+  // cfg3 +4 %, xall +3 %, r50x8 -1 %, configs[3] layout -2 %; 296 x 1 and 592 x 1 slower
+  // (profiles/r02/sweep_tail_keep_4gpu.txt, one run each, within the box spread), so 0.
   static const int tail_env = env_int("RP_XGPU_TAIL", 0);
-  const int64_t nsmall = std::min<int64_t>(std::max(0, tail_env), tiles / 4);
-  const int64_t tb = tiles - nsmall;
+  static const int tail_w = std::max(1, env_int("RP_XGPU_TAIL_TILES", 1));
+  static const int tail_keep = env_int("RP_XGPU_TAIL_KEEP", 0);
+  const int64_t nsmall = std::min<int64_t>(std::max(0, tail_env), tiles / (4 * tail_w));
+  const int64_t tb = tiles - nsmall * tail_w;
   int64_t nch = static_cast<int64_t>(kXLanes) * iters;
   nch = std::min<int64_t>(nch, std::max<int64_t>(1, tb / min_tiles));
   nch = std::min<int64_t>(nch, kMaxChunks - nsmall);
   if (nch > kXLanes) nch = nch / kXLanes * kXLanes;  // whole rounds of lanes
+  if (tail_keep && nsmall > 0 && nch - nsmall >= kXLanes) nch -= nsmall;
   p.CH = tb;
-  p.nsmall = nsmall;
+  p.nsmall = static_cast<int32_t>(nsmall);
+  p.tail_w = tail_w;
   p.nch = std::max<int64_t>(1, nch) + nsmall;
 }
 

@@ -195,10 +195,10 @@ __device__ __forceinline__ int64_t slice_lo(const XPart& p, int o) { return min(
 __device__ __forceinline__ Range chunk_range(const XPart& p, int o, int64_t c) {
   const int64_t slo = slice_lo(p, o), shi = min(static_cast<int64_t>(o + 1) * p.S4, p.n4);
   Range r;
-  // balanced big chunks: tiles [c CH / nbig, (c+1) CH / nbig); then nsmall one-tile chunks
+  // balanced big chunks: tiles [c CH / nbig, (c+1) CH / nbig); then nsmall chunks of tail_w tiles
   const int64_t nbig = p.nch - p.nsmall;
-  const int64_t t_lo = c < nbig ? (c * p.CH) / nbig : p.CH + (c - nbig);
-  const int64_t t_hi = c < nbig ? ((c + 1) * p.CH) / nbig : t_lo + 1;
+  const int64_t t_lo = c < nbig ? (c * p.CH) / nbig : p.CH + (c - nbig) * p.tail_w;
+  const int64_t t_hi = c < nbig ? ((c + 1) * p.CH) / nbig : t_lo + p.tail_w;
   r.lo = min(slo + t_lo * 1024, shi);
   r.hi = min(slo + t_hi * 1024, shi);
   r.tail = (o == p.kp - 1) && (c == p.nch - 1) && p.rem > 0;
