@@ -173,7 +173,32 @@ def test_emulated_suite_with_poisoned_staging():
         pytest.skip("needs a GPU")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_emulated.py"), "-q",
-                        "-m", "gpu", "-x", "-p", "no:cacheprovider", "-k", "not poisoned and not full_r50"],
+                        "-m", "gpu", "-x", "-p", "no:cacheprovider", "-k",
+                        "not poisoned and not full_r50 and not variant"],
                        capture_output=True, text=True, cwd=root, timeout=900,
                        env={**os.environ, "RP_DEBUG_POISON": "1"})
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [
+    {"RP_XGPU_EARLY_A": "0"},                       # A flags at the iteration's end
+    {"RP_XGPU_LOOKAHEAD": "1"},                     # next A block pushed while B waits
+    {"RP_XGPU_TAIL": "296", "RP_XGPU_TAIL_TILES": "2", "RP_XGPU_TAIL_KEEP": "1"},   # small last chunks
+    {"RP_XGPU_SIG2": "0", "RP_XGPU_BLAG": "3"},     # one SIG per iteration, static lanes
+    {"RP_XGPU_CLAIM": "part"},                      # part-major claiming for GG steps too
+], ids=["late_a", "lookahead", "tail", "sig1", "part_major"])
+def test_emulated_suite_pipeline_variant(env):
+    # the off-by-default flag-pipeline variants of the cross kernel (kept as measured experiments,
+    # DESIGN.md §6) stay correct: the emulated suite with poisoned staging under each of them
+    import os
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_emulated.py"), "-q",
+                        "-m", "gpu", "-x", "-p", "no:cacheprovider", "-k",
+                        "not poisoned and not full_r50 and not variant"],
+                       capture_output=True, text=True, cwd=root, timeout=900,
+                       env={**os.environ, "RP_DEBUG_POISON": "1", **env})
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
