@@ -1,0 +1,6 @@
+# round 2, call ai (1 GPU): HEAD after the geometry-struct change -- smoke(), pytest -m gpu (incl. the
+# pipeline-variant suites), bench N=1
+OUT=gpurun_out/r02ai; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1; echo "rc=$?" >> $OUT/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/pytest_gpu_1gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_1gpu.log
+timeout 600 python bench.py > $OUT/bench_n1.json 2> $OUT/bench_n1.err
