@@ -904,15 +904,18 @@ void xgpu_geometry(XPart& p, int64_t n) {
   // and the slowest lane sets the kernel time); chunks of >= kMinTiles tiles on average, at most
   // kMaxChunks. RP_XGPU_ITERS / RP_XGPU_MIN_TILES override (tuning; every rank of a job must see
   // the same values: the geometry must agree across GPUs)
-  // Default: about 4 tiles (64 KB) per chunk, 3..6 chunks per lane -- ResNet-50 slices take 3
-  // chunks per lane, VGG-16 slices 6 (6 gave +7 % at VGG size, 3 was best at ResNet-50 size and
-  // 2 lost 12 % on the 8-worker problem at N = 4: profiles/r02/sweep_dyn_2gpu.txt, r02/final_4gpu/).
+  // Default: about 4 tiles (64 KB) per chunk, 2..6 chunks per lane -- ResNet-50 slices take 2-3
+  // chunks per lane, VGG-16 slices 6 (6 gave +7 % at VGG size: profiles/r02/sweep_dyn_2gpu.txt).
+  // The floor was 3 while A flags were posted at the iteration's end (2 lost 12 % on the 8-worker
+  // problem at N = 4, r02/final_4gpu/); with early A flags 2 is as good or better at ResNet-50 size
+  // (N = 4, medians of three alternated runs: r50x8 18,055 vs 17,300, cfg3 14,611 vs 14,519;
+  // profiles/r02/sweep_iters_early_a_4gpu*.txt).
   static const int iters_env = env_int("RP_XGPU_ITERS", 0);
   static const int min_tiles = std::max(1, env_int("RP_XGPU_MIN_TILES", kMinTiles));
   const int64_t tiles = p.S4 / kTileF4;
   const int iters = iters_env > 0 ? iters_env
                                   : static_cast<int>(std::max<int64_t>(
-                                        3, std::min<int64_t>(6, (tiles + kXLanes * 3) / (kXLanes * 4))));
+                                        2, std::min<int64_t>(6, (tiles + kXLanes * 3) / (kXLanes * 4))));
   // RP_XGPU_TAIL = t > 0 (experiment, off): the last t chunks are RP_XGPU_TAIL_TILES tiles each
   // (default 1), taken last under dynamic claiming to shorten the kernel's tail; RP_XGPU_TAIL_KEEP=1
   // takes them out of the big chunks' count (same number of chunks, so the same flag overhead).
