@@ -863,7 +863,8 @@ int sig2_setting() {  // RP_XGPU_SIG2: two SIG jobs per lane iteration in the wa
   return v;
 }
 int blag_setting() {  // RP_XGPU_BLAG: iterations between a chunk's A and B stages (tuning)
-  // one SIG per iteration: >= 2, 3 best (profiles/r02/sweep_blag_2gpu.txt); two SIGs: >= 1
+  // one SIG per iteration: >= 2, 3 best (profiles/r02/sweep_blag_2gpu.txt); two SIGs: >= 1, 1 best
+  // (2 with early A flags measured one 1.5 ms/step cfg3 run at N = 4, profiles/r02/sweep_iters_early_a_4gpu.txt)
   static const int v = std::max(sig2_setting() ? 1 : 2, std::min(6, env_int("RP_XGPU_BLAG", sig2_setting() ? 1 : 3)));
   return v;
 }
