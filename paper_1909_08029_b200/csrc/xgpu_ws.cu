@@ -1,9 +1,10 @@
 // Cross-GPU fused SGD + P-Reduce, warp-specialized (default for plain-SGD steps, fp32 and bf16).
 //
-// Same method, geometry, work order and flag protocol as xgpu.cu (read its header first): a
-// group on GPUs d_0 < ... < d_{kp-1} is a reduce-scatter + all-gather fused with alg1 step 2
-// and the pre-reduction of co-resident members (reading R1); chunk c runs on lane
-// c mod kXLanes; a lane is the pipeline {A(c_i), B(c_{i-2}), C(c_{i-4}), signal(i-1)}.
+// Same method, chunk geometry and flag words as xgpu.cu (read its header first): a group on GPUs
+// d_0 < ... < d_{kp-1} is a reduce-scatter + all-gather fused with alg1 step 2 and the
+// pre-reduction of co-resident members (reading R1). By default CTAs claim chunks dynamically and
+// run the iteration structure described under "Flags" below; without a claim counter chunk c
+// runs on lane c mod kXLanes in xgpu.cu's static lane pipeline.
 //
 // What changes is how a CTA moves the bytes. Round 2 measured the LDG/STG version per CTA
 // (RP_XGPU_PROFILE breakdown, profiles/r02/): 65-96 % of a CTA's time went to loading x, g and
